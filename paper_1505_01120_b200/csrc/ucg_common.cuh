@@ -1,0 +1,89 @@
+// ucg_common.cuh — shared internals of libucores_cuda.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "ucores_cuda.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libucores_cuda targets sm_100a only"
+#endif
+
+namespace ucg {
+
+// ---- error state ------------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+int check_device();  // UCG_OK when the current device is compute capability 10.x
+int sm_count();      // SMs of the current device (cached per device)
+extern std::atomic<uint64_t> g_launches;
+
+#define UCG_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return ::ucg::cuda_fail(_e, #call); \
+  } while (0)
+
+// after a <<<>>> launch
+#define UCG_LAUNCHED()                                          \
+  do {                                                          \
+    ::ucg::g_launches.fetch_add(1, std::memory_order_relaxed);  \
+    cudaError_t _e = cudaGetLastError();                        \
+    if (_e != cudaSuccess) return ::ucg::cuda_fail(_e, "kernel launch"); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- device helpers -----------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t umin(uint64_t a, uint64_t b) { return a < b ? a : b; }
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// The two reduce combines. SUM: IEEE a+b (identity -0.0f, exact for every
+// operand); MAX: std::max(a,b) == (a<b)?b:a (identity -inf as right operand).
+struct OpSum {
+  static __device__ __forceinline__ float apply(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float identity() { return -0.0f; }
+  static __device__ __forceinline__ float empty() { return 0.0f; }
+};
+struct OpMax {
+  static __device__ __forceinline__ float apply(float a, float b) { return (a < b) ? b : a; }
+  static __device__ __forceinline__ float identity() { return __int_as_float(0xff800000); }
+  static __device__ __forceinline__ float empty() { return __int_as_float(0xff800000); }
+};
+
+// streaming 128-bit global accesses (data is touched exactly once)
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+
+}  // namespace ucg
+
+// segment table (opaque to C callers)
+struct ucg_segtab {
+  int device;
+  uint64_t nseg;
+  uint64_t nitems;         // work items over all segments
+  uint64_t* d_begin;       // [nseg]
+  uint64_t* d_len;         // [nseg]
+  uint64_t* d_first_item;  // [nseg+1]
+  uint32_t* d_item_seg;    // [nitems]
+  uint64_t max_items_per_seg;
+};
+
+namespace ucg {
+// Work item = one aligned block of kItemFloats floats of one segment
+// (the last item of a segment may be partial).
+constexpr int kItemLog2 = 14;
+constexpr uint64_t kItemFloats = 1ull << kItemLog2;
+}  // namespace ucg

@@ -1,0 +1,119 @@
+// ucg_pi.cu — Monte-Carlo pi device op, workload C3.
+//
+// Per sample gid of task t: s0 = seed ^ gid*GAMMA, z1 = mix64(s0+GAMMA),
+// z2 = mix64(s0+2*GAMMA), a = z1>>32, b = z2>>32, and the reference test is
+//   fl(fl(x*x) + fl(y*y)) <= 1.0   with x = a/2^32, y = b/2^32 in IEEE double.
+// Here x*x = fl(a^2)*2^-64 exactly, so the test is decided in integers from
+// the exact S = a^2 + b^2 (65 bits): the double evaluation differs from S by
+// less than 2^13, hence S <= 2^64 - 2^14 is a certain hit and S >= 2^64 + 2^14
+// a certain miss; the band in between (probability ~1e-15) re-evaluates the
+// exact double expression with __dmul_rn / __dadd_rn (no FMA contraction).
+// Counts: ballot-free integer accumulation, warp redux, one 64-bit atomic per
+// CTA per 64Ki-sample work unit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ucg_common.cuh"
+
+namespace ucg {
+namespace {
+
+constexpr int kPiThreads = 256;
+constexpr int kUnitLog2 = 16;  // samples per work unit
+constexpr int kMaxTasks = 512; // per launch
+
+struct PiTasks {
+  uint64_t seed[kMaxTasks];
+  uint64_t samples[kMaxTasks];
+  uint64_t first_unit[kMaxTasks + 1];
+  uint32_t ntasks;
+};
+
+__device__ __forceinline__ uint32_t pi_hit(uint64_t s0) {
+  const uint64_t z1 = mix64(s0 + kGamma);
+  const uint64_t z2 = mix64(s0 + 2 * kGamma);
+  const uint32_t a = uint32_t(z1 >> 32), b = uint32_t(z2 >> 32);
+  const uint64_t A = uint64_t(a) * a, B = uint64_t(b) * b;
+  const uint64_t lo = A + B;
+  const bool carry = lo < A;
+  if (!carry && lo < 0xFFFFFFFFFFFFC000ull) return 1u;  // S <= 2^64 - 2^14
+  if (carry && lo >= (1ull << 14)) return 0u;           // S >= 2^64 + 2^14
+  const double x = double(a) * (1.0 / 4294967296.0);
+  const double y = double(b) * (1.0 / 4294967296.0);
+  return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)) <= 1.0 ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTasks tasks, uint64_t nunits,
+                                                   unsigned long long* __restrict__ hits) {
+  __shared__ uint32_t warp_sum[kPiThreads / 32];
+  for (uint64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+    // task owning this unit: binary search over first_unit
+    uint32_t lo = 0, hi = tasks.ntasks;  // first_unit[lo] <= unit < first_unit[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (tasks.first_unit[mid] <= unit) lo = mid;
+      else hi = mid;
+    }
+    const uint64_t seed = tasks.seed[lo];
+    const uint64_t base = (unit - tasks.first_unit[lo]) << kUnitLog2;
+    const uint64_t end = umin(tasks.samples[lo], base + (1ull << kUnitLog2));
+    uint32_t cnt = 0;
+    uint64_t gid = base + threadIdx.x;
+    uint64_t m = gid * kGamma;
+    const uint64_t mstep = uint64_t(kPiThreads) * kGamma;
+    if (end - base == (1ull << kUnitLog2)) {
+#pragma unroll 4
+      for (int i = 0; i < (1 << kUnitLog2) / kPiThreads; ++i) {
+        cnt += pi_hit(seed ^ m);
+        m += mstep;
+      }
+    } else {
+      for (; gid < end; gid += kPiThreads) {
+        cnt += pi_hit(seed ^ m);
+        m += mstep;
+      }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < kPiThreads / 32; ++w) t += warp_sum[w];
+      atomicAdd(hits + lo, t);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace ucg
+
+using namespace ucg;
+
+extern "C" int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
+                           void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!ntasks) return UCG_OK;
+  if (!seeds || !samples || !hits_out) return fail(UCG_ERR_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  UCG_CUDA(cudaMemsetAsync(hits_out, 0, ntasks * sizeof(int64_t), st));
+  for (uint64_t t0 = 0; t0 < ntasks; t0 += kMaxTasks) {
+    const uint32_t nt = uint32_t(std::min<uint64_t>(kMaxTasks, ntasks - t0));
+    PiTasks p;
+    p.ntasks = nt;
+    p.first_unit[0] = 0;
+    for (uint32_t i = 0; i < nt; ++i) {
+      p.seed[i] = seeds[t0 + i];
+      p.samples[i] = samples[t0 + i];
+      p.first_unit[i + 1] = p.first_unit[i] + ((samples[t0 + i] + (1ull << kUnitLog2) - 1) >> kUnitLog2);
+    }
+    const uint64_t nunits = p.first_unit[nt];
+    if (!nunits) continue;
+    const unsigned grid = unsigned(std::min<uint64_t>(nunits, uint64_t(sm_count()) * 8));
+    k_pi<<<grid, kPiThreads, 0, st>>>(p, nunits, reinterpret_cast<unsigned long long*>(hits_out + t0));
+    UCG_LAUNCHED();
+  }
+  return UCG_OK;
+}

@@ -1,0 +1,311 @@
+// ucg_runtime.cu — device runtime of libucores_cuda.so: error state, device
+// enumeration (the GPU half of ucores/device.hpp:212-242), memory, streams,
+// events, synthetic-input fills and segment tables.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ucg_common.cuh"
+
+namespace ucg {
+
+static thread_local std::string t_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  t_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  t_last_error = std::string(what) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? UCG_ERR_NODEV : UCG_ERR_CUDA;
+}
+
+namespace {
+struct DevCache {
+  int sms = 0;
+  int major = 0;
+};
+std::mutex g_dev_mu;
+DevCache g_dev[64];
+
+const DevCache* dev_cache(int* dev_out) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  *dev_out = dev;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_dev[dev].sms == 0) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return nullptr;
+    g_dev[dev].sms = p.multiProcessorCount;
+    g_dev[dev].major = p.major;
+  }
+  return &g_dev[dev];
+}
+}  // namespace
+
+int check_device() {
+  int dev = -1;
+  const DevCache* c = dev_cache(&dev);
+  if (!c) {
+    cudaGetLastError();
+    return fail(UCG_ERR_NODEV, "no usable CUDA device (libucores_cuda has no CPU fallback)");
+  }
+  if (c->major != 10) {
+    return fail(UCG_ERR_NODEV, "device " + std::to_string(dev) +
+                                   " is not compute capability 10.x (built for sm_100a only)");
+  }
+  return UCG_OK;
+}
+
+int sm_count() {
+  int dev = -1;
+  const DevCache* c = dev_cache(&dev);
+  return c ? c->sms : 148;
+}
+
+// ---- fills -------------------------------------------------------------------
+__global__ void k_fill_uniform(float* __restrict__ out, uint64_t n, uint64_t seed, uint64_t first) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    out[i] = float(mix64(seed + (first + i + 1) * kGamma) >> 40) * (1.0f / 16777216.0f);
+  }
+}
+__global__ void k_fill_bytes(uint8_t* __restrict__ out, uint64_t n, uint64_t seed, uint64_t first) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    out[i] = uint8_t(mix64(seed + (first + i + 1) * kGamma) >> 56);
+  }
+}
+
+// ---- segment table -------------------------------------------------------------
+}  // namespace ucg
+
+using namespace ucg;
+
+extern "C" {
+
+const char* ucg_last_error(void) { return t_last_error.c_str(); }
+int ucg_abi_version(void) { return UCG_ABI_VERSION; }
+
+int ucg_device_count(int* n_out) {
+  if (!n_out) return fail(UCG_ERR_ARG, "n_out is null");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *n_out = 0;
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return UCG_OK;
+    return cuda_fail(e, "cudaGetDeviceCount");
+  }
+  *n_out = n;
+  return UCG_OK;
+}
+
+int ucg_device_info_get(int ordinal, ucg_device_info* out) {
+  if (!out) return fail(UCG_ERR_ARG, "out is null");
+  cudaDeviceProp p;
+  UCG_CUDA(cudaGetDeviceProperties(&p, ordinal));
+  std::memset(out, 0, sizeof *out);
+  std::strncpy(out->name, p.name, sizeof out->name - 1);
+  out->ordinal = ordinal;
+  out->cc_major = p.major;
+  out->cc_minor = p.minor;
+  out->sm_count = p.multiProcessorCount;
+  out->hbm_bytes = p.totalGlobalMem;
+  out->l2_bytes = p.l2CacheSize;
+  return UCG_OK;
+}
+
+int ucg_set_device(int ordinal) {
+  UCG_CUDA(cudaSetDevice(ordinal));
+  return UCG_OK;
+}
+
+int ucg_malloc(void** dptr, uint64_t bytes) {
+  if (!dptr) return fail(UCG_ERR_ARG, "dptr is null");
+  *dptr = nullptr;
+  if (bytes == 0) return UCG_OK;
+  UCG_CUDA(cudaMalloc(dptr, bytes));
+  return UCG_OK;
+}
+int ucg_free(void* dptr) {
+  if (dptr) UCG_CUDA(cudaFree(dptr));
+  return UCG_OK;
+}
+int ucg_host_alloc(void** hptr, uint64_t bytes) {
+  if (!hptr) return fail(UCG_ERR_ARG, "hptr is null");
+  *hptr = nullptr;
+  if (bytes == 0) return UCG_OK;
+  UCG_CUDA(cudaHostAlloc(hptr, bytes, cudaHostAllocPortable));
+  return UCG_OK;
+}
+int ucg_host_free(void* hptr) {
+  if (hptr) UCG_CUDA(cudaFreeHost(hptr));
+  return UCG_OK;
+}
+int ucg_host_register(void* hptr, uint64_t bytes) {
+  if (!hptr || !bytes) return UCG_OK;
+  UCG_CUDA(cudaHostRegister(hptr, bytes, cudaHostRegisterPortable));
+  return UCG_OK;
+}
+int ucg_host_unregister(void* hptr) {
+  if (hptr) UCG_CUDA(cudaHostUnregister(hptr));
+  return UCG_OK;
+}
+int ucg_memcpy_h2d(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (!bytes) return UCG_OK;
+  UCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+  return UCG_OK;
+}
+int ucg_memcpy_d2h(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (!bytes) return UCG_OK;
+  UCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+  return UCG_OK;
+}
+int ucg_memcpy_d2d(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (!bytes) return UCG_OK;
+  UCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
+  return UCG_OK;
+}
+int ucg_memset(void* dst, int value, uint64_t bytes, void* stream) {
+  if (!bytes) return UCG_OK;
+  UCG_CUDA(cudaMemsetAsync(dst, value, bytes, as_stream(stream)));
+  return UCG_OK;
+}
+int ucg_stream_create(void** s) {
+  if (!s) return fail(UCG_ERR_ARG, "stream_out is null");
+  cudaStream_t st;
+  UCG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *s = st;
+  return UCG_OK;
+}
+int ucg_stream_destroy(void* s) {
+  if (s) UCG_CUDA(cudaStreamDestroy(as_stream(s)));
+  return UCG_OK;
+}
+int ucg_stream_synchronize(void* s) {
+  UCG_CUDA(cudaStreamSynchronize(as_stream(s)));
+  return UCG_OK;
+}
+int ucg_event_create(void** ev) {
+  if (!ev) return fail(UCG_ERR_ARG, "ev_out is null");
+  cudaEvent_t e;
+  UCG_CUDA(cudaEventCreate(&e));
+  *ev = e;
+  return UCG_OK;
+}
+int ucg_event_destroy(void* ev) {
+  if (ev) UCG_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev)));
+  return UCG_OK;
+}
+int ucg_event_record(void* ev, void* stream) {
+  UCG_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), as_stream(stream)));
+  return UCG_OK;
+}
+int ucg_stream_wait_event(void* stream, void* ev) {
+  UCG_CUDA(cudaStreamWaitEvent(as_stream(stream), reinterpret_cast<cudaEvent_t>(ev), 0));
+  return UCG_OK;
+}
+int ucg_event_elapsed_ms(void* a, void* b, float* ms) {
+  if (!ms) return fail(UCG_ERR_ARG, "ms_out is null");
+  UCG_CUDA(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(b)));
+  UCG_CUDA(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(a), reinterpret_cast<cudaEvent_t>(b)));
+  return UCG_OK;
+}
+int ucg_device_synchronize(void) {
+  UCG_CUDA(cudaDeviceSynchronize());
+  return UCG_OK;
+}
+uint64_t ucg_launch_count(void) { return g_launches.load(); }
+
+int ucg_fill_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t first, void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!n) return UCG_OK;
+  if (!out) return fail(UCG_ERR_ARG, "out is null");
+  const unsigned grid = unsigned(sm_count()) * 8;
+  k_fill_uniform<<<grid, 256, 0, as_stream(stream)>>>(out, n, seed, first);
+  UCG_LAUNCHED();
+  return UCG_OK;
+}
+int ucg_fill_bytes_u8(uint8_t* out, uint64_t n, uint64_t seed, uint64_t first, void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!n) return UCG_OK;
+  if (!out) return fail(UCG_ERR_ARG, "out is null");
+  const unsigned grid = unsigned(sm_count()) * 8;
+  k_fill_bytes<<<grid, 256, 0, as_stream(stream)>>>(out, n, seed, first);
+  UCG_LAUNCHED();
+  return UCG_OK;
+}
+
+int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg, ucg_segtab** out) {
+  if (!out) return fail(UCG_ERR_ARG, "out is null");
+  *out = nullptr;
+  if (int rc = check_device()) return rc;
+  if (nseg && (!begin || !len)) return fail(UCG_ERR_ARG, "begin/len is null");
+  if (nseg >= (1ull << 32)) return fail(UCG_ERR_ARG, "too many segments");
+  std::vector<uint64_t> first(nseg + 1, 0);
+  uint64_t maxi = 0;
+  for (uint64_t s = 0; s < nseg; ++s) {
+    if (begin[s] % 4) return fail(UCG_ERR_ARG, "segment " + std::to_string(s) + " begin is not 16-byte aligned");
+    const uint64_t items = (len[s] + kItemFloats - 1) >> kItemLog2;
+    first[s + 1] = first[s] + items;
+    if (items > maxi) maxi = items;
+  }
+  const uint64_t nitems = first[nseg];
+  std::vector<uint32_t> item_seg(nitems);
+  for (uint64_t s = 0; s < nseg; ++s)
+    for (uint64_t i = first[s]; i < first[s + 1]; ++i) item_seg[i] = uint32_t(s);
+  auto* t = new ucg_segtab{};
+  cudaGetDevice(&t->device);
+  t->nseg = nseg;
+  t->nitems = nitems;
+  t->max_items_per_seg = maxi;
+  auto cleanup = [&](cudaError_t e, const char* what) {
+    cudaFree(t->d_begin);
+    cudaFree(t->d_len);
+    cudaFree(t->d_first_item);
+    cudaFree(t->d_item_seg);
+    delete t;
+    return cuda_fail(e, what);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&t->d_begin, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMalloc(&t->d_len, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMalloc(&t->d_first_item, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if (nseg) {
+    if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
+    if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
+  }
+  if ((e = cudaMemcpy(t->d_first_item, first.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
+  if (nitems && (e = cudaMemcpy(t->d_item_seg, item_seg.data(), nitems * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cleanup(e, "cudaMemcpy");
+  *out = t;
+  return UCG_OK;
+}
+
+int ucg_segtab_destroy(ucg_segtab* t) {
+  if (!t) return UCG_OK;
+  cudaFree(t->d_begin);
+  cudaFree(t->d_len);
+  cudaFree(t->d_first_item);
+  cudaFree(t->d_item_seg);
+  delete t;
+  return UCG_OK;
+}
+
+int ucg_segtab_scratch_floats(const ucg_segtab* t, uint64_t* n_out) {
+  if (!t || !n_out) return fail(UCG_ERR_ARG, "null argument");
+  *n_out = t->nitems + 1;
+  return UCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+"""Typed wrappers over the C-ABI for torch-owned device memory.
+
+Each wrapper names the reference operation it implements. Tensors must live on
+the current CUDA device; work is enqueued on the current torch stream (or the
+`stream` given), so CUDA events recorded by torch bracket it correctly.
+"""
+from __future__ import annotations
+
+from typing import Sequence
+
+import ctypes as C
+
+from . import capi
+from .capi import call, ptr, stream_handle, u64_array
+
+
+def _require_cuda(*ts) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise capi.DeviceUnavailable("tensor is not on a CUDA device (no CPU fallback)")
+
+
+def fill_uniform_(out, seed: int, first: int = 0, stream=None):
+    """Synthetic U[0,1) input: out[i] = (mix64(seed + (first+i+1)*GAMMA) >> 40) * 2^-24."""
+    _require_cuda(out)
+    call("ucg_fill_uniform_f32", ptr(out), out.numel(), seed, first, stream_handle(stream))
+    return out
+
+
+def fill_bytes_(out, seed: int, first: int = 0, stream=None):
+    _require_cuda(out)
+    call("ucg_fill_bytes_u8", ptr(out), out.numel(), seed, first, stream_handle(stream))
+    return out
+
+
+def map_affine(x, y, a: float, b: float, n: int | None = None, stream=None):
+    """axpb mapCL body (engine.hpp:54-85): y = fl(fl(a*x)+b)."""
+    _require_cuda(x, y)
+    call("ucg_map_affine_f32", ptr(x), ptr(y), x.numel() if n is None else n, a, b, stream_handle(stream))
+    return y
+
+
+def elementwise2(a, b, c, op: str = "sum", stream=None):
+    """Fig-3 vectoradd body c = a (op) b (sum2 / max2 / isum2)."""
+    _require_cuda(a, b, c)
+    if a.numel() != b.numel():
+        raise capi.LengthMismatch("vector lengths differ")
+    import torch
+
+    if a.dtype == torch.int64:
+        call("ucg_elementwise2_i64", ptr(a), ptr(b), ptr(c), a.numel(), stream_handle(stream))
+    else:
+        call("ucg_elementwise2_f32", ptr(a), ptr(b), ptr(c), a.numel(), capi.OPS[op], stream_handle(stream))
+    return c
+
+
+def segment_reduce(x, segtab: capi.SegTab, op: str, scratch, out, stream=None):
+    """mapCLPartition psum/pmax over every segment (engine.hpp:89-114)."""
+    _require_cuda(x, scratch, out)
+    call("ucg_segment_reduce_f32", ptr(x), segtab.handle, capi.OPS[op], ptr(scratch), ptr(out),
+         stream_handle(stream))
+    return out
+
+
+def map_affine_segment_reduce(x, y, segtab: capi.SegTab, a: float, b: float, op: str, scratch, out, stream=None):
+    """Fused mapCL(axpb) -> mapCLPartition(psum|pmax): y written, partials reduced."""
+    _require_cuda(x, y, scratch, out)
+    call("ucg_map_affine_segment_reduce_f32", ptr(x), ptr(y), segtab.handle, a, b, capi.OPS[op], ptr(scratch),
+         ptr(out), stream_handle(stream))
+    return out
+
+
+def tree_reduce(x, n: int, op: str, out, stream=None):
+    """reduceCL stage 2 over n one-float partials (engine.hpp:172-190)."""
+    _require_cuda(x, out)
+    call("ucg_tree_reduce_f32", ptr(x), n, capi.OPS[op], ptr(out), stream_handle(stream))
+    return out
+
+
+def reduce_cl_vectors(elem_ptrs, count: int, length: int, part_counts: Sequence[int], op: str, out, dtype="f32",
+                      stream=None):
+    """Full reduceCL (stage 1 folds + stage 2 tree) over vector elements.
+
+    elem_ptrs: int64 CUDA tensor holding the device addresses of the elements.
+    """
+    _require_cuda(elem_ptrs, out)
+    pc = u64_array(part_counts)
+    if dtype == "i64":
+        call("ucg_reduce_cl_i64", ptr(elem_ptrs), count, length, pc, len(part_counts), ptr(out),
+             stream_handle(stream))
+    else:
+        call("ucg_reduce_cl_f32", ptr(elem_ptrs), count, length, pc, len(part_counts), capi.OPS[op], ptr(out),
+             stream_handle(stream))
+    return out
+
+
+def pi_hits(seeds: Sequence[int], samples: Sequence[int], hits_out, stream=None):
+    """Monte-Carlo pi mapCL over tasks {seed, samples}."""
+    _require_cuda(hits_out)
+    call("ucg_pi_hits", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out), stream_handle(stream))
+    return hits_out
+
+
+def sobel_bands(inp, in_off: Sequence[int], out, out_off: Sequence[int], rows: Sequence[int], width: int,
+                stream=None):
+    """mapCLPartition sobel over row bands (one launch for all bands)."""
+    _require_cuda(inp, out)
+    call("ucg_sobel_bands_u8", ptr(inp), u64_array(in_off), ptr(out), u64_array(out_off), u64_array(rows),
+         len(rows), width, stream_handle(stream))
+    return out
+
+
+def gemm_tf32(A, B, Cm, n: int, stream=None):
+    _require_cuda(A, B, Cm)
+    call("ucg_gemm_tf32", ptr(A), ptr(B), ptr(Cm), n, stream_handle(stream))
+    return Cm

@@ -1,0 +1,153 @@
+"""Device-resident mapCL -> mapCLPartition -> reduceCL pipeline over a sharded
+collection (BASELINE configs 1 and 2).
+
+Reference semantics (ucores/engine.hpp):
+  y  = map_cl(x, "axpb")               :54-85   one task per element
+  ps = map_cl_partition(y, "psum")     :89-114  one task per partition (concat)
+  r  = reduce_cl(ps, "sum2")           :121-192 stage 2 tree over P partials
+
+Layout in HBM: every partition's concatenated payload is one segment starting
+at a 256-byte aligned float offset of one buffer (x and y share the layout).
+Sharding: rank g of G holds partitions [gP/G, (g+1)P/G);
+the only exchange is an all-gather of the per-partition partials (NCCL via
+torch.distributed), after which every rank runs the reference stage-2 tree
+over all P partials in partition order — bit-identical to one GPU.
+
+With fused=True the map and the partition reduction run as ONE kernel (read
+x, write y, reduce y: 8 B/elem instead of 12); y is still materialised, so
+the outputs are identical to the unfused chain.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import capi, ops
+
+ALIGN_FLOATS = 64  # 256-byte segment alignment
+
+
+def partition_sizes(n: int, num_partitions: int) -> list[int]:
+    """create_dataset ceiling-first sizes (ucores/dataset.hpp:64-82)."""
+    if num_partitions < 1:
+        from .errors import InvalidPartitionCount
+
+        raise InvalidPartitionCount(f"num_partitions must be >= 1, got {num_partitions}")
+    base, extra = divmod(n, num_partitions)
+    return [base + (1 if p < extra else 0) for p in range(num_partitions)]
+
+
+def shard_range(num_partitions: int, world: int, rank: int) -> range:
+    """Contiguous block of partitions owned by `rank` (partition p -> GPU floor(p*G/P))."""
+    lo = (rank * num_partitions) // world
+    hi = ((rank + 1) * num_partitions) // world
+    return range(lo, hi)
+
+
+@dataclass
+class Layout:
+    """Segment layout of a set of partitions in one device buffer."""
+
+    lens: list[int]
+    begins: list[int]
+    total: int
+
+    @classmethod
+    def of(cls, lens: list[int], align: int = ALIGN_FLOATS) -> "Layout":
+        begins, off = [], 0
+        for n in lens:
+            begins.append(off)
+            off += (n + align - 1) // align * align
+        return cls(list(lens), begins, max(off, align))
+
+
+class MapReducePipeline:
+    """One rank's share of the C1/C2 pipeline, inputs resident in HBM."""
+
+    def __init__(self, part_lens: list[int], a: float = 2.0, b: float = 1.0, op: str = "sum",
+                 fused: bool = True, world: int = 1, rank: int = 0, device: torch.device | None = None,
+                 seed_base: int = 1000, plant_max: bool = True, group=None):
+        self.P = len(part_lens)
+        self.part_lens = list(part_lens)
+        self.a, self.b, self.op, self.fused = float(a), float(b), op, fused
+        self.world, self.rank, self.group = world, rank, group
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.owned = shard_range(self.P, world, rank)
+        self.local_lens = [self.part_lens[p] for p in self.owned]
+        self.layout = Layout.of(self.local_lens)
+        self.elements = sum(self.part_lens)
+        self.local_elements = sum(self.local_lens)
+        dev = self.device
+        self.x = torch.empty(self.layout.total, dtype=torch.float32, device=dev)
+        self.y = torch.empty_like(self.x)
+        self.segtab = capi.SegTab(self.layout.begins, self.local_lens)
+        self.scratch = torch.empty(max(1, self.segtab.scratch_floats), dtype=torch.float32, device=dev)
+        self.partials = torch.empty(max(1, len(self.local_lens)), dtype=torch.float32, device=dev)
+        self.max_local = max(len(shard_range(self.P, world, r)) for r in range(world))
+        self.gather_buf = torch.empty(world * max(1, self.max_local), dtype=torch.float32, device=dev)
+        self.send_buf = torch.empty(max(1, self.max_local), dtype=torch.float32, device=dev)
+        idx = []
+        for r in range(world):
+            rr = shard_range(self.P, world, r)
+            idx.extend(r * self.max_local + k for k in range(len(rr)))
+        self.gather_index = torch.tensor(idx, dtype=torch.int64, device=dev)
+        self.all_partials = torch.empty(max(1, self.P), dtype=torch.float32, device=dev)
+        self.result = torch.empty(1, dtype=torch.float32, device=dev)
+        self.seed_base = seed_base
+        self.plant_max = plant_max
+        self.fill()
+
+    # -- synthetic input: partition p ~ U[0,1) from seed seed_base+p --------------
+    def fill(self) -> None:
+        for k, p in enumerate(self.owned):
+            n = self.local_lens[k]
+            if n:
+                seg = self.x[self.layout.begins[k]: self.layout.begins[k] + n]
+                ops.fill_uniform_(seg, self.seed_base + p)
+                if self.plant_max and p == self.P // 2:
+                    seg[n // 3] = 1.5  # the unique planted maximum
+
+    def host_input(self) -> list:
+        """This rank's partitions as host arrays (for oracle checks)."""
+        out = []
+        for k in range(len(self.local_lens)):
+            b, n = self.layout.begins[k], self.local_lens[k]
+            out.append(self.x[b:b + n].cpu().numpy())
+        return out
+
+    def local_output(self, k: int) -> torch.Tensor:
+        b = self.layout.begins[k]
+        return self.y[b:b + self.local_lens[k]]
+
+    # -- one step ---------------------------------------------------------------
+    def map_and_partials(self, stream=None) -> None:
+        if self.fused:
+            ops.map_affine_segment_reduce(self.x, self.y, self.segtab, self.a, self.b, self.op, self.scratch,
+                                          self.partials, stream=stream)
+        else:
+            ops.map_affine(self.x, self.y, self.a, self.b, stream=stream)
+            ops.segment_reduce(self.y, self.segtab, self.op, self.scratch, self.partials, stream=stream)
+
+    def combine(self, stream=None) -> torch.Tensor:
+        """reduce_cl stage 2 over all P partials (exchange first when sharded)."""
+        if self.world == 1:
+            ops.tree_reduce(self.partials, self.P, self.op, self.result, stream=stream)
+            return self.result
+        import torch.distributed as dist
+
+        n = len(self.local_lens)
+        self.send_buf.fill_(0.0)
+        if n:
+            self.send_buf[:n].copy_(self.partials[:n])
+        dist.all_gather_into_tensor(self.gather_buf, self.send_buf, group=self.group)
+        torch.index_select(self.gather_buf, 0, self.gather_index, out=self.all_partials)
+        ops.tree_reduce(self.all_partials, self.P, self.op, self.result, stream=stream)
+        return self.result
+
+    def step(self) -> torch.Tensor:
+        self.map_and_partials()
+        return self.combine()
+
+    def close(self) -> None:
+        self.segtab.close()

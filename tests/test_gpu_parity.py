@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference golden vectors. Integer / index / max / map results and — because
+the kernels reproduce the reference pairing tree exactly — fp32 sums are all
+compared BIT-EXACT; full-size C2 additionally checks fp32 sums against fp64
+at rel 1e-5 (BASELINE.json north_star tolerance)."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _bits(t):
+    a = t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+    return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+# ---- map -------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 127, 4096, 1000003])
+def test_map_affine_bitexact(cuda, n):
+    from paper_1505_01120_b200 import ops
+
+    x = O.fill_uniform(77, n) * np.float32(8) - np.float32(4)
+    xd = torch.from_numpy(x).to(cuda)
+    yd = torch.empty_like(xd)
+    ops.map_affine(xd, yd, 2.0, 1.0)
+    ops.map_affine(xd, xd, 0.3, -7.25) if n else None  # in-place form
+    torch.cuda.synchronize()
+    assert np.array_equal(_bits(yd), O.map_affine(x, 2.0, 1.0).view(np.uint32))
+    assert np.array_equal(_bits(xd), O.map_affine(x, 0.3, -7.25).view(np.uint32))
+
+
+# ---- partition reductions ----------------------------------------------------------
+
+SEG_LENS = [0, 1, 2, 3, 4, 5, 31, 127, 128, 129, 1023, 1024, 1025, 16383, 16384, 16385, 40000, 100003, 262144]
+
+
+def _segments(lens, seed=5, signed_zeros=False):
+    from paper_1505_01120_b200.pipeline import Layout
+
+    lay = Layout.of(lens)
+    buf = np.full(lay.total, np.nan, np.float32)  # padding poison must never leak in
+    host = []
+    for k, n in enumerate(lens):
+        v = (O.fill_uniform(seed + k, n) * np.float32(2) - np.float32(1)).astype(np.float32)
+        if signed_zeros and n:
+            v[::5] = np.float32(0.0)
+            v[1::5] = np.float32(-0.0)
+        buf[lay.begins[k]: lay.begins[k] + n] = v
+        host.append(v)
+    return lay, buf, host
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+@pytest.mark.parametrize("signed_zeros", [False, True])
+def test_segment_reduce_bitexact(cuda, op, signed_zeros):
+    from paper_1505_01120_b200 import capi, ops
+
+    lay, buf, host = _segments(SEG_LENS, signed_zeros=signed_zeros)
+    x = torch.from_numpy(buf).to(cuda)
+    tab = capi.SegTab(lay.begins, SEG_LENS)
+    scratch = torch.empty(tab.scratch_floats, dtype=torch.float32, device=cuda)
+    out = torch.empty(len(SEG_LENS), dtype=torch.float32, device=cuda)
+    ops.segment_reduce(x, tab, op, scratch, out)
+    want = np.array([O.tree_reduce(h, op) for h in host], np.float32)
+    assert np.array_equal(_bits(out), want.view(np.uint32))
+    tab.close()
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_fused_map_reduce_bitexact(cuda, op):
+    from paper_1505_01120_b200 import capi, ops
+
+    lay, buf, host = _segments(SEG_LENS, seed=11)
+    x = torch.from_numpy(buf).to(cuda)
+    y = torch.full_like(x, 123.0)
+    tab = capi.SegTab(lay.begins, SEG_LENS)
+    scratch = torch.empty(tab.scratch_floats, dtype=torch.float32, device=cuda)
+    out = torch.empty(len(SEG_LENS), dtype=torch.float32, device=cuda)
+    ops.map_affine_segment_reduce(x, y, tab, 2.0, 1.0, op, scratch, out)
+    yh = y.cpu().numpy()
+    for k, h in enumerate(host):
+        want_y = O.map_affine(h, 2.0, 1.0)
+        got_y = yh[lay.begins[k]: lay.begins[k] + len(h)]
+        assert np.array_equal(got_y.view(np.uint32), want_y.view(np.uint32))
+        assert _bits(out)[k] == np.float32(O.tree_reduce(want_y, op)).view(np.uint32)
+    # padding between segments is never written
+    for k, n in enumerate(SEG_LENS[:-1]):
+        gap = yh[lay.begins[k] + n: lay.begins[k + 1]]
+        assert np.all(gap == 123.0)
+    tab.close()
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 7, 64, 1000, 2048, 2049, 5000, 70001])
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_tree_reduce_bitexact(cuda, n, op):
+    from paper_1505_01120_b200 import ops
+
+    x = (O.fill_uniform(n + 3, n) - np.float32(0.5)).astype(np.float32)
+    out = torch.empty(1, dtype=torch.float32, device=cuda)
+    ops.tree_reduce(torch.from_numpy(x).to(cuda) if n else torch.empty(1, device=cuda), n, op, out)
+    assert _bits(out)[0] == np.float32(O.tree_reduce(x, op)).view(np.uint32)
+
+
+# ---- reduce_cl over vectors (stage-1 folds + stage-2 tree) -------------------------
+
+def _reduce_cl_gpu(cuda, elems, counts, op="sum"):
+    from paper_1505_01120_b200 import ops
+
+    dt = torch.int64 if elems.dtype == np.int64 else torch.float32
+    # elements as separate device buffers (arbitrary addresses, like a Dataset)
+    bufs = [torch.from_numpy(np.ascontiguousarray(e)).to(cuda) for e in elems]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=cuda)
+    out = torch.empty(elems.shape[1], dtype=dt, device=cuda)
+    ops.reduce_cl_vectors(ptrs, elems.shape[0], elems.shape[1], counts, op, out,
+                          dtype="i64" if dt == torch.int64 else "f32")
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def test_reduce_cl_isum_golden(cuda, golden):
+    from test_oracle_golden import _isum_cases
+
+    for case, elems, parts in _isum_cases(golden):
+        counts = O.partition_sizes(elems.shape[0], parts)
+        assert _reduce_cl_gpu(cuda, elems, counts).tolist() == case["result"]
+
+
+def test_reduce_cl_fig3_and_acceptance2(cuda, golden):
+    out = _reduce_cl_gpu(cuda, np.array([[1, 2, 3], [4, 5, 6]], np.float32), [2])
+    assert out.tolist() == [5.0, 7.0, 9.0]
+    n, P = 1 << 20, 8
+    elems = np.stack([O.fill_vectoradd(k, n) for k in range(P)])
+    out = _reduce_cl_gpu(cuda, elems, [1] * P)
+    assert O.fnv64(out) == golden["vectoradd_acc2"]["fnv"]
+    assert "%.3f" % float(out.astype(np.float64).sum()) == golden["vectoradd_acc2"]["checksum"]
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_reduce_cl_ragged_float(cuda, op):
+    rng = np.random.default_rng(3)
+    for trial in range(6):
+        count = int(rng.integers(1, 60))
+        parts = int(rng.integers(1, 20))
+        length = int(rng.integers(1, 3000))
+        elems = rng.standard_normal((count, length)).astype(np.float32)
+        elems[:, ::7] = -0.0
+        counts = O.partition_sizes(count, parts)
+        got = _reduce_cl_gpu(cuda, elems, counts, op)
+        assert np.array_equal(got.view(np.uint32), O.reduce_cl(elems, counts, op).view(np.uint32))
+
+
+def test_reduce_cl_empty_raises(cuda):
+    from paper_1505_01120_b200 import EmptyDataset, ops
+
+    out = torch.empty(4, dtype=torch.float32, device=cuda)
+    ptrs = torch.empty(1, dtype=torch.int64, device=cuda)
+    with pytest.raises(EmptyDataset):
+        ops.reduce_cl_vectors(ptrs, 0, 4, [0, 0], "sum", out)
+
+
+# ---- pipelines at the BASELINE shapes ------------------------------------------------
+
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("key", ["c1", "c1_ragged"])
+def test_c1_pipeline_golden(cuda, golden, fused, key):
+    """C1: 2^20 fp32 as 4 elements in 4 partitions, map_cl(axpb) -> map_cl_partition(psum|pmax) -> reduce_cl."""
+    from paper_1505_01120_b200 import ops
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    g = golden[key]
+    n, P, E = g["n"], g["partitions"], g["elements"]
+    # element k of n//E(+1); partition p holds a contiguous run of elements
+    esz = O.partition_sizes(n, E)
+    counts = O.partition_sizes(E, P)
+    part_lens, pos = [], 0
+    for c in counts:
+        part_lens.append(sum(esz[pos:pos + c]))
+        pos += c
+    for op in ("sum", "max"):
+        pipe = MapReducePipeline(part_lens, op=op, fused=fused, plant_max=False)
+        # overwrite the synthetic fill with the C1 collection (one stream, seed 12345)
+        first = 0
+        for k, ln in enumerate(part_lens):
+            seg = pipe.x[pipe.layout.begins[k]: pipe.layout.begins[k] + ln]
+            ops.fill_uniform_(seg, 12345, first)
+            first += ln
+        r = pipe.step()
+        torch.cuda.synchronize()
+        ys = np.concatenate([pipe.local_output(k).cpu().numpy() for k in range(P)])
+        assert O.fnv64(ys) == g["y_fnv"]
+        assert [O.f32_bits(v) for v in pipe.partials.cpu().numpy()[:P]] == g["partials_" + op]
+        assert O.f32_bits(r.cpu().numpy()[0]) == g["total_" + op]
+        pipe.close()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_c2_small_golden(cuda, golden, fused):
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    g = golden["c2_small"]
+    for op in ("sum", "max"):
+        pipe = MapReducePipeline([g["L"]] * g["P"], op=op, fused=fused)
+        r = pipe.step()
+        ys = np.concatenate([pipe.local_output(k).cpu().numpy() for k in range(g["P"])])
+        assert O.fnv64(ys) == g["y_fnv"]
+        assert [O.f32_bits(v) for v in pipe.partials.cpu().numpy()] == g["partials_" + op]
+        assert O.f32_bits(r.cpu().numpy()[0]) == g["total_" + op]
+        pipe.close()
+
+
+@pytest.mark.slow
+def test_c2_full_size(cuda):
+    """C2 at the BASELINE size (2^30 fp32, 64 partitions): size-independent checks."""
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    P, L = 64, 1 << 24
+    pipe = MapReducePipeline([L] * P, op="sum", fused=True)
+    r = float(pipe.step().item())
+    partials = pipe.partials.cpu().numpy()
+    rng = np.random.default_rng(0)
+    total64 = 0.0
+    for p in range(P):
+        y = pipe.local_output(p).cpu().numpy()
+        if p in (0, 17, P // 2, P - 1):  # exact tree on a sample of partitions
+            assert O.f32_bits(O.tree_reduce(y, "sum")) == O.f32_bits(partials[p])
+            idx = rng.integers(0, L, 4096)
+            x = np.array([O.fill_uniform(1000 + p, 1, int(i))[0] for i in idx], np.float32)
+            if p == P // 2:
+                x[idx == L // 3] = 1.5
+            assert np.array_equal(y[idx].view(np.uint32), O.map_affine(x, 2.0, 1.0).view(np.uint32))
+        s64 = float(y.astype(np.float64).sum())
+        assert abs(float(partials[p]) - s64) / s64 < 1e-5
+        total64 += s64
+    assert O.f32_bits(O.tree_reduce(partials, "sum")) == O.f32_bits(np.float32(r))
+    assert abs(r - total64) / total64 < 1e-5
+    # max: the planted maximum 1.5 maps to exactly 4.0
+    pipe2 = MapReducePipeline([L] * P, op="max", fused=False)
+    assert float(pipe2.step().item()) == 4.0
+    pipe.close()
+    pipe2.close()
+
+
+# ---- pi / sobel ------------------------------------------------------------------------
+
+def test_pi_golden(cuda, golden):
+    from paper_1505_01120_b200 import ops
+
+    for case in golden["pi"]:
+        S, T, seed = case["samples"], case["tasks"], case["seed"]
+        samples = [S // T + (1 if t < S % T else 0) for t in range(T)]
+        hits = torch.empty(T, dtype=torch.int64, device=cuda)
+        ops.pi_hits([seed + t for t in range(T)], samples, hits)
+        assert hits.cpu().tolist() == case["task_hits"]
+
+
+def test_pi_vs_oracle_small(cuda):
+    from paper_1505_01120_b200 import ops
+
+    seeds = [0, 1, 2**63 + 5, 2**64 - 1, 42]
+    samples = [0, 1, 65535, 65536, 200001]
+    hits = torch.empty(len(seeds), dtype=torch.int64, device=cuda)
+    ops.pi_hits(seeds, samples, hits)
+    assert hits.cpu().tolist() == [O.pi_hits(s, n) for s, n in zip(seeds, samples)]
+
+
+def test_sobel_golden_and_random(cuda, golden):
+    from paper_1505_01120_b200 import ops
+
+    g = golden["sobel"]
+    # (W=40 golden: generic path; multiples of 16: the vectorised path)
+    for (H, W, rows, seed) in [(g["H"], g["W"], g["rows"], g["seed"]), (50, 48, 16, 7), (64, 256, 32, 3),
+                               (37, 1024, 5, 9), (300, 528, 64, 1), (70, 33, 9, 2)]:
+        img = O.sobel_image(H, W, seed)
+        bands = O.sobel_bands(img, rows)
+        inp = np.concatenate([b.ravel() for b in bands])
+        in_off, out_off, rws = [], [], []
+        pi = po = 0
+        for b in bands:
+            in_off.append(pi)
+            out_off.append(po)
+            rws.append(b.shape[0] - 2)
+            pi += b.size
+            po += (b.shape[0] - 2) * W
+        dinp = torch.from_numpy(inp).to(cuda)
+        dout = torch.zeros(po, dtype=torch.uint8, device=cuda)
+        ops.sobel_bands(dinp, in_off, dout, out_off, rws, W)
+        want = np.concatenate([O.sobel_band(b, b.shape[0] - 2, W) for b in bands])
+        got = dout.cpu().numpy()
+        assert np.array_equal(got, want)
+        if (H, W) == (g["H"], g["W"]):
+            assert O.fnv64(got) == g["fnv"]
