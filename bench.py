@@ -1,0 +1,342 @@
+"""bench.py — BASELINE.json headline: mapCL + reduceCL elements/s on B200.
+
+Workload (BASELINE configs[1], "C2"): a collection of 2^30 fp32 elements in 64
+partitions of 2^24, one pass of
+    y  = map_cl(x, "axpb")            (y = 2x + 1)
+    ps = map_cl_partition(y, "psum")  (per-partition pairing-tree sum)
+    r  = reduce_cl(ps, "sum2")        (reference stage-2 tree over 64 partials)
+per step, partitions sharded over the N GPUs (strong scaling: the collection
+is fixed). `value` = 2^30 / device step time (max over ranks, CUDA events,
+inputs resident in HBM, 4 GiB per GPU at N=1 > L2). `e2e` = the same step
+with the shard uploaded every step from pinned host memory (overlapped
+chunk-wise with the kernel) and the result read back.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--no-fuse] [--op sum|max] [--parts P] [--part-len L]
+
+--impl reference times the reference's own CPU implementation (the
+unmodified ucores headers compiled into oracle/_ref/ref_harness: Engine +
+WorkerRuntime + HostParallelExecutor over all host threads) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "mapCL+reduceCL elements/sec and % HBM roofline at 1/2/4/8 B200 vs host CPU"
+UNIT = "elements/s"
+REF_HARNESS = ROOT / "oracle" / "_ref" / "ref_harness"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+PROFILE_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--op", default="sum", choices=["sum", "max"])
+    ap.add_argument("--parts", type=int, default=64)
+    ap.add_argument("--part-len", type=int, default=1 << 24)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-parts", type=int, default=4)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---- reference arm / cpu baseline --------------------------------------------------
+
+def run_ref_harness(parts: int, part_len: int, steps: int, warmup: int, op: str, threads: int) -> dict:
+    if not REF_HARNESS.exists():
+        raise RuntimeError(f"{REF_HARNESS} missing (build it with `make -C oracle ref` where the reference exists)")
+    cmd = [str(REF_HARNESS), "bench", "--parts", str(parts), "--part-len", str(part_len), "--threads",
+           str(threads), "--steps", str(steps), "--warmup", str(warmup), "--op", op]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=1800).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    parts = args.cpu_sample_parts
+    r = run_ref_harness(parts, args.part_len, args.steps, args.warmup, args.op, threads)
+    elems = r["elements"]
+    step = statistics.median(r["step_s"])
+    value = elems / step
+    sample = (f"{parts} partitions x {args.part_len} fp32 ({elems} elements; same partition size as the "
+              f"{args.parts}-partition workload), {r['executor']} width {threads}, {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args, world=1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result_bits": r["result_bits"],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- clocks --------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self._t = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        try:
+            for line in self.proc.stdout:
+                self.rows.append([c.strip() for c in line.split(",")])
+        except Exception:
+            pass
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self._t.join(timeout=5)
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---- our arm ------------------------------------------------------------------------
+
+def workload_config(args, world: int) -> dict:
+    n = args.parts * args.part_len
+    return {
+        "workload": (f"C2: map_cl(axpb) -> map_cl_partition(p{args.op}) -> reduce_cl({args.op}2) over "
+                     f"{n} fp32 elements in {args.parts} partitions of {args.part_len}"),
+        "elements": n, "partitions": args.parts, "part_len": args.part_len,
+        "fused": not args.no_fuse,
+        "fusion": "map+partition-reduce in one kernel, y materialised" if not args.no_fuse else "none",
+        "sharding": f"partition blocks over {world} GPU(s); NCCL all-gather of {args.parts} partials",
+        "l2": f"inputs larger than L2 ({n * 4 // world / 2**30:.2f} GiB x per GPU)",
+    }
+
+
+def load_peak() -> tuple[float, str]:
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(key: str):
+    try:
+        return json.loads(PROFILE_SUMMARY.read_text()).get(key)
+    except Exception:
+        return None
+
+
+def our_arm(args, world, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1505_01120_b200 import capi
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    capi.load()
+    lens = [args.part_len] * args.parts
+    pipe = MapReducePipeline(lens, op=args.op, fused=not args.no_fuse, world=world, rank=rank, device=dev,
+                             group=group)
+    n_total = pipe.elements
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    k = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        # warm-up (>= 3 steps) plus an untimed soak of ~1 s so the clock record
+        # reflects steady state; the sampler keeps running through the timed region
+        for _ in range(max(3, args.warmup)):
+            pipe.step()
+        barrier()
+        soak_end = time.perf_counter() + 1.0
+        while time.perf_counter() < soak_end:
+            for _ in range(10):
+                pipe.step()
+            torch.cuda.synchronize()
+        launches0 = capi.launch_count()
+        barrier()
+        t0.record()
+        for i in range(k):
+            ev[i][0].record()
+            pipe.map_and_partials()
+            ev[i][1].record()
+            pipe.combine()
+        t1.record()
+        barrier()
+    launches = capi.launch_count() - launches0
+    step_ms = t0.elapsed_time(t1) / k
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    result = float(pipe.result.item())
+
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, kern_ms = float(t[0]), float(t[1])
+
+    # ---- e2e: host buffers, H2D/D2H inside the timed region -------------------------
+    pipe.setup_host_input()
+    for _ in range(2):
+        pipe.step_from_host()
+    barrier()
+    e0 = time.perf_counter()
+    te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    te0.record()
+    for _ in range(args.e2e_steps):
+        r_host = pipe.step_from_host()
+    te1.record()
+    barrier()
+    e2e_ms = te0.elapsed_time(te1) / args.e2e_steps
+    wall_e2e_ms = (time.perf_counter() - e0) * 1e3 / args.e2e_steps
+    h2d = pipe.h2d_bytes
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_ms, float(h2d)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+        hb = torch.tensor([float(h2d)], dtype=torch.float64, device=dev)
+        dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+        h2d = int(hb.item())
+    assert r_host == result or (r_host != r_host and result != result), (r_host, result)
+
+    # ---- roofline of the dominant kernel (fused map + partition reduce) --------------
+    local_elems = pipe.local_elements
+    bytes_per_elem = 8 if not args.no_fuse else 12  # fused: read x + write y; unfused adds the y re-read
+    algo_bytes = bytes_per_elem * local_elems
+    achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
+    peak, peak_kind = load_peak()
+    traffic = load_traffic("fused_pass1_bytes_per_launch" if not args.no_fuse else "unfused_bytes_per_step")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            r = run_ref_harness(args.cpu_sample_parts, args.part_len, 1, 0, args.op, threads)
+            cpu = {"value": r["elements"] / statistics.median(r["step_s"]), "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": (f"{args.cpu_sample_parts} partitions x {args.part_len} fp32 ({r['elements']} elements), "
+                              f"unmodified ucores Engine+WorkerRuntime+{r['executor']} width {threads}, {cpu_model()}")}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        value = n_total / (step_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (counter-hash U[0,1), partition p seeded 1000+p, planted max)",
+            "config": workload_config(args, world),
+            "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 4 * world, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": ("ucg_map_affine_segment_reduce_f32 (pass1+pass2)" if not args.no_fuse
+                                    else "ucg_map_affine_f32 + ucg_segment_reduce_f32"),
+                         "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": kern_ms,
+                         "peak_kind": peak_kind, "frac_of_8TBs": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "result": result,
+        }
+        print(json.dumps(line), flush=True)
+    pipe.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+    return our_arm(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

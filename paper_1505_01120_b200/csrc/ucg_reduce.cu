@@ -14,13 +14,14 @@
 // Operands are always combined as op(left, right) (std::max is not
 // commutative on signed zeros).
 //
-// Data movement: one warp owns a work item of 2^14 floats of one segment and
-// streams it in 1024-float chunks (8 coalesced LDG.128 per lane, 16 KB per
-// chunk per warp in flight). A chunk is reduced with a value-halving
-// butterfly: 12 shuffles per 1024 floats instead of 40.
+// Data movement: one warp owns a work item of 2^14 contiguous floats of one
+// segment and streams it in chunks of 128*U floats (U coalesced LDG.128 per
+// lane in flight). A chunk is reduced with a value-halving butterfly
+// (U-1 + 5 shuffles per chunk instead of 5U).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ucg_common.cuh"
@@ -40,18 +41,46 @@ __device__ __forceinline__ float affine(float x, float a, float b) {
   return __fadd_rn(__fmul_rn(a, x), b);
 }
 
-// Reduce one 1024-float chunk at `x` (16B aligned). Lane l holds floats
-// [128u + 4l, 128u + 4l + 4) of sub-block u (u = 0..7). kGuard: only the
-// first `valid` floats exist (the rest are the identity). kMap: the chunk is
-// first mapped through y = fl(fl(a*x)+b) and the mapped values are stored to
-// y before being reduced. Returns the chunk's tree value in every lane.
-template <class Op, bool kMap, bool kGuard>
-__device__ __forceinline__ float chunk1024(const float* __restrict__ x, float* __restrict__ y,
-                                           int64_t valid, float a, float b, int lane) {
-  float s[8];
-  float4 v[8];
+// Tree over the U per-lane values of one chunk of 128*U floats at x (16B
+// aligned). Lane l holds floats [128u + 4l, 128u + 4l + 4) of sub-block u.
+// Value-halving butterfly: at lane bit j (j < log2 U) a lane keeps half of
+// its values and trades the other half with lane l^(1<<j), so U values cost
+// U-1 shuffles instead of 5U; afterwards lane l holds sub-block
+// bitreverse(l & (U-1)), finished across the remaining lane bits, and the U
+// sub-block roots are combined by the final xor levels.
+template <class Op, int U>
+__device__ __forceinline__ float warp_chunk_tree(float (&s)[U], int lane) {
+  constexpr int H = U == 8 ? 3 : (U == 4 ? 2 : (U == 2 ? 1 : 0));
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int j = 0; j < H; ++j) {
+    const int cnt = U >> j;
+    const bool hi = (lane >> j) & 1;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; ++i) {
+      const float keep = hi ? s[i + cnt / 2] : s[i];
+      const float send = hi ? s[i] : s[i + cnt / 2];
+      s[i] = lr<Op>(keep, __shfl_xor_sync(kFull, send, 1 << j), !hi);
+    }
+  }
+  float r = s[0];
+#pragma unroll
+  for (int j = H; j < 5; ++j) r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1 << j), !((lane >> j) & 1));
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    const int bit = H - 1 - k;  // sub-block index bit k lives in lane bit H-1-k
+    r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1 << bit), !((lane >> bit) & 1));
+  }
+  return r;
+}
+
+// One chunk of 128*U floats, in two halves so loads of the next chunk can
+// be in flight while the current one is reduced. kGuard: only the first
+// `valid` floats exist (the rest are the identity). kMap: the chunk is mapped
+// through y = fl(fl(a*x)+b), stored to y, and the mapped values are reduced.
+template <class Op, bool kGuard, int U>
+__device__ __forceinline__ void chunk_load(const float* __restrict__ x, int64_t valid, int lane, float4 (&v)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
     const int off = 128 * u + 4 * lane;
     if (!kGuard || off + 3 < valid) {
       v[u] = ld_stream(reinterpret_cast<const float4*>(x + off));
@@ -63,8 +92,15 @@ __device__ __forceinline__ float chunk1024(const float* __restrict__ x, float* _
       v[u].w = off + 3 < valid ? x[off + 3] : id;
     }
   }
+}
+
+// Returns the chunk's tree value in every lane.
+template <class Op, bool kMap, bool kGuard, int U>
+__device__ __forceinline__ float chunk_finish(float4 (&v)[U], float* __restrict__ y, int64_t valid, float a,
+                                              float b, int lane) {
+  float s[U];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int u = 0; u < U; ++u) {
     const int off = 128 * u + 4 * lane;
     if (kMap) {
       if (!kGuard || off + 3 < valid) {
@@ -83,77 +119,77 @@ __device__ __forceinline__ float chunk1024(const float* __restrict__ x, float* _
     }
     s[u] = Op::apply(Op::apply(v[u].x, v[u].y), Op::apply(v[u].z, v[u].w));
   }
-  // value-halving butterfly over lane bits 0,1,2 (8-, 16-, 32-float nodes)
-  const bool b0 = lane & 1, b1 = lane & 2, b2 = lane & 4;
-  float t[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float keep = b0 ? s[j + 4] : s[j];
-    const float send = b0 ? s[j] : s[j + 4];
-    t[j] = lr<Op>(keep, __shfl_xor_sync(kFull, send, 1), !b0);
-  }
-  float q[2];
-#pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const float keep = b1 ? t[j + 2] : t[j];
-    const float send = b1 ? t[j] : t[j + 2];
-    q[j] = lr<Op>(keep, __shfl_xor_sync(kFull, send, 2), !b1);
-  }
-  float r;
-  {
-    const float keep = b2 ? q[1] : q[0];
-    const float send = b2 ? q[0] : q[1];
-    r = lr<Op>(keep, __shfl_xor_sync(kFull, send, 4), !b2);
-  }
-  // lane now holds sub-block (4*b0 + 2*b1 + b2) over its 8-lane group; finish
-  // the 64- and 128-float nodes across lane bits 3, 4.
-  r = lr<Op>(r, __shfl_xor_sync(kFull, r, 8), !(lane & 8));
-  r = lr<Op>(r, __shfl_xor_sync(kFull, r, 16), !(lane & 16));
-  // tree over the 8 sub-blocks: (u, u^1) differ in lane bit 2, then bit 1, then bit 0
-  r = lr<Op>(r, __shfl_xor_sync(kFull, r, 4), !b2);
-  r = lr<Op>(r, __shfl_xor_sync(kFull, r, 2), !b1);
-  r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1), !b0);
-  return r;
+  return warp_chunk_tree<Op, U>(s, lane);
 }
 
-// Reduce one work item: `valid` floats at x (<= kItemFloats), as 16 chunks
-// combined by a binary-counter stack (aligned power-of-two subtrees).
-template <class Op, bool kMap>
-__device__ __forceinline__ float work_item(const float* __restrict__ x, float* __restrict__ y,
-                                           int64_t valid, float a, float b, int lane) {
-  constexpr int kChunks = int(kItemFloats / 1024);
-  constexpr int kDepth = kItemLog2 - 10;
-  float stk[kDepth];
+// Binary-counter merge of chunk c's root into the register stack.
+template <class Op, int D>
+__device__ __forceinline__ void counter_push(float (&stk)[D], float& v, int c) {
+  bool carry = true;
 #pragma unroll
-  for (int j = 0; j < kDepth; ++j) stk[j] = Op::identity();
-  float v = Op::identity();
-  const bool full = valid >= int64_t(kItemFloats);
-#pragma unroll 1
-  for (int c = 0; c < kChunks; ++c) {
-    const int64_t rem = valid - int64_t(c) * 1024;
-    if (full || rem >= 1024) {
-      v = chunk1024<Op, kMap, false>(x + c * 1024, y + c * 1024, 1024, a, b, lane);
-    } else if (rem > 0) {
-      v = chunk1024<Op, kMap, true>(x + c * 1024, y + c * 1024, rem, a, b, lane);
-    } else {
-      v = Op::identity();
-    }
-#pragma unroll
-    for (int j = 0; j < kDepth; ++j) {
+  for (int j = 0; j < D; ++j) {
+    if (carry) {
       if (c & (1 << j)) {
         v = Op::apply(stk[j], v);
       } else {
         stk[j] = v;
-        break;
+        carry = false;
       }
     }
   }
-  return v;  // c = kChunks-1 has all bits set: v is the root
 }
 
-// Pass 1: one warp per work item (grid-stride over items).
-template <class Op, bool kMap>
-__global__ void __launch_bounds__(kWarps * 32)
+// Reduce one work item: `valid` floats at x (<= kItemFloats) as
+// kItemFloats/(128U) chunks merged by a binary-counter stack of aligned
+// power-of-two subtrees (register-resident: every index is static). Full
+// items are software-pipelined: chunk c+1 is loaded before chunk c is reduced.
+template <class Op, bool kMap, int U>
+__device__ __forceinline__ float work_item(const float* __restrict__ x, float* __restrict__ y,
+                                           int64_t valid, float a, float b, int lane) {
+  constexpr int kChunk = 128 * U;
+  constexpr int kChunks = int(kItemFloats / kChunk);
+  constexpr int kDepth = (kChunks >= 64 ? 6 : kChunks >= 32 ? 5 : kChunks >= 16 ? 4 : kChunks >= 8 ? 3 : 2);
+  float stk[kDepth];
+#pragma unroll
+  for (int j = 0; j < kDepth; ++j) stk[j] = Op::identity();
+  float v = Op::identity();
+  if (valid >= int64_t(kItemFloats)) {
+    float4 cur[U], nxt[U];
+    chunk_load<Op, false, U>(x, kChunk, lane, cur);
+#pragma unroll 1
+    for (int c = 0; c < kChunks; ++c) {
+      if (c + 1 < kChunks) chunk_load<Op, false, U>(x + (c + 1) * kChunk, kChunk, lane, nxt);
+      v = chunk_finish<Op, kMap, false, U>(cur, y + c * kChunk, kChunk, a, b, lane);
+      counter_push<Op, kDepth>(stk, v, c);
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
+    return v;  // c = kChunks-1 has all bits set: v is the root
+  }
+#pragma unroll 1
+  for (int c = 0; c < kChunks; ++c) {
+    const int64_t rem = valid - int64_t(c) * kChunk;
+    if (rem >= kChunk) {
+      float4 cur[U];
+      chunk_load<Op, false, U>(x + c * kChunk, kChunk, lane, cur);
+      v = chunk_finish<Op, kMap, false, U>(cur, y + c * kChunk, kChunk, a, b, lane);
+    } else if (rem > 0) {
+      float4 cur[U];
+      chunk_load<Op, true, U>(x + c * kChunk, rem, lane, cur);
+      v = chunk_finish<Op, kMap, true, U>(cur, y + c * kChunk, rem, a, b, lane);
+    } else {
+      v = Op::identity();
+    }
+    counter_push<Op, kDepth>(stk, v, c);
+  }
+  return v;
+}
+
+// Pass 1: one warp per work item (grid-stride over items). U = 4 keeps the
+// kernel under 40 registers so 6 CTAs (48 warps) stay resident per SM —
+// enough 16-byte loads in flight to cover HBM latency at full bandwidth.
+template <class Op, bool kMap, int U, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_segment_pass1(const float* __restrict__ x, float* __restrict__ y, const uint64_t* __restrict__ begin,
                     const uint64_t* __restrict__ len, const uint64_t* __restrict__ first_item,
                     const uint32_t* __restrict__ item_seg, uint64_t nitems, float a, float b,
@@ -166,7 +202,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     const uint64_t blk = item - first_item[s];
     const uint64_t off = begin[s] + (blk << kItemLog2);
     const int64_t valid = int64_t(umin(kItemFloats, len[s] - (blk << kItemLog2)));
-    const float r = work_item<Op, kMap>(x + off, kMap ? y + off : nullptr, valid, a, b, lane);
+    const float r = work_item<Op, kMap, U>(x + off, kMap ? y + off : nullptr, valid, a, b, lane);
     if (lane == 0) partial[item] = r;
   }
 }
@@ -347,18 +383,50 @@ __global__ void __launch_bounds__(128) k_reduce_cl(const T* const* __restrict__ 
   out[j] = acc;
 }
 
+// Pass-1 variants (chunk width U, CTAs per SM). The default was chosen by a
+// sweep on B200 (tools/microbench.py); UCG_PASS1_VARIANT overrides it for
+// tuning runs.
+struct Pass1Variant {
+  int u, minb;
+};
+constexpr Pass1Variant kPass1Variants[] = {{8, 2}, {4, 3}, {4, 4}, {2, 8}, {2, 6}, {8, 3}};
+constexpr int kPass1Default = 0;
+
+inline int pass1_variant() {
+  static int v = [] {
+    const char* e = getenv("UCG_PASS1_VARIANT");
+    int k = e ? atoi(e) : kPass1Default;
+    return (k < 0 || k >= int(sizeof(kPass1Variants) / sizeof(kPass1Variants[0]))) ? kPass1Default : k;
+  }();
+  return v;
+}
+
+template <class Op, bool kMap, int U, int MINB>
+void launch_pass1(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, cudaStream_t st) {
+  const uint64_t want = (t->nitems + kWarps - 1) / kWarps;
+  const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(sm_count()) * MINB));
+  k_segment_pass1<Op, kMap, U, MINB><<<grid, kWarps * 32, 0, st>>>(x, y, t->d_begin, t->d_len, t->d_first_item,
+                                                                  t->d_item_seg, t->nitems, a, b, scratch);
+}
+
+template <class Op, bool kMap>
+void dispatch_pass1(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, cudaStream_t st) {
+  switch (pass1_variant()) {
+    case 1: launch_pass1<Op, kMap, 4, 3>(x, y, t, a, b, scratch, st); break;
+    case 2: launch_pass1<Op, kMap, 4, 4>(x, y, t, a, b, scratch, st); break;
+    case 3: launch_pass1<Op, kMap, 2, 8>(x, y, t, a, b, scratch, st); break;
+    case 4: launch_pass1<Op, kMap, 2, 6>(x, y, t, a, b, scratch, st); break;
+    case 5: launch_pass1<Op, kMap, 8, 3>(x, y, t, a, b, scratch, st); break;
+    default: launch_pass1<Op, kMap, 8, 2>(x, y, t, a, b, scratch, st); break;
+  }
+}
+
 template <class Op>
 int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, float* out,
                    cudaStream_t st) {
   if (t->nitems) {
-    const uint64_t want = (t->nitems + kWarps - 1) / kWarps;
-    const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(sm_count()) * 4));
-    if (y)
-      k_segment_pass1<Op, true><<<grid, kWarps * 32, 0, st>>>(x, y, t->d_begin, t->d_len, t->d_first_item,
-                                                             t->d_item_seg, t->nitems, a, b, scratch);
-    else
-      k_segment_pass1<Op, false><<<grid, kWarps * 32, 0, st>>>(x, y, t->d_begin, t->d_len, t->d_first_item,
-                                                              t->d_item_seg, t->nitems, a, b, scratch);
+    if (y) dispatch_pass1<Op, true>(x, y, t, a, b, scratch, st);
+    else dispatch_pass1<Op, false>(x, y, t, a, b, scratch, st);
     UCG_LAUNCHED();
   }
   if (t->nseg) {

@@ -149,5 +149,50 @@ class MapReducePipeline:
         self.map_and_partials()
         return self.combine()
 
+    # -- end to end: inputs from pinned host memory, result back to the host ------
+    def setup_host_input(self, chunks: int = 8) -> None:
+        """Pinned host copy of this rank's input + per-chunk segment tables so
+        the upload of chunk c+1 (copy stream) overlaps the kernel on chunk c."""
+        self.host_x = torch.empty(self.layout.total, dtype=torch.float32, pin_memory=True)
+        self.host_x.copy_(self.x)
+        self.host_result = torch.empty(1, dtype=torch.float32, pin_memory=True)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        nloc = len(self.local_lens)
+        chunks = max(1, min(chunks, nloc))
+        self.groups = []
+        for c in range(chunks):
+            k0, k1 = (c * nloc) // chunks, ((c + 1) * nloc) // chunks
+            if k0 == k1:
+                continue
+            xb = self.layout.begins[k0]
+            xe = self.layout.begins[k1 - 1] + (self.local_lens[k1 - 1] + ALIGN_FLOATS - 1) // ALIGN_FLOATS * ALIGN_FLOATS
+            tab = capi.SegTab([self.layout.begins[k] - xb for k in range(k0, k1)], self.local_lens[k0:k1])
+            scratch = torch.empty(max(1, tab.scratch_floats), dtype=torch.float32, device=self.device)
+            self.groups.append((k0, k1, xb, xe, tab, scratch))
+        self.h2d_bytes = sum((xe - xb) * 4 for (_, _, xb, xe, _, _) in self.groups)
+
+    def step_from_host(self) -> float:
+        """One end-to-end step: H2D of the shard, map+reduce, combine, D2H of the result."""
+        cur = torch.cuda.current_stream(self.device)
+        self.copy_stream.wait_stream(cur)  # previous step finished reading x
+        for (k0, k1, xb, xe, tab, scratch) in self.groups:
+            with torch.cuda.stream(self.copy_stream):
+                self.x[xb:xe].copy_(self.host_x[xb:xe], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+            cur.wait_event(ev)
+            if self.fused:
+                ops.map_affine_segment_reduce(self.x[xb:], self.y[xb:], tab, self.a, self.b, self.op, scratch,
+                                              self.partials[k0:])
+            else:
+                ops.map_affine(self.x[xb:xe], self.y[xb:xe], self.a, self.b)
+                ops.segment_reduce(self.y[xb:], tab, self.op, scratch, self.partials[k0:])
+        r = self.combine()
+        self.host_result.copy_(r, non_blocking=True)
+        cur.synchronize()
+        return float(self.host_result[0])
+
     def close(self) -> None:
         self.segtab.close()
+        for g in getattr(self, "groups", []):
+            g[4].close()

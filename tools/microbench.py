@@ -1,5 +1,6 @@
 """Kernel micro-benchmarks (CUDA events, warm-up, inputs > L2). Dev tool."""
 import json
+import os
 import sys
 
 import torch
@@ -54,6 +55,10 @@ def main():
     pipe.close()
     del pipe, y2
     torch.cuda.empty_cache()
+    if "--quick" in sys.argv:
+        res["variant"] = os.environ.get("UCG_PASS1_VARIANT", "default")
+        print(json.dumps(res))
+        return
     # pi 2^34 / 64 tasks
     T = 64
     hits = torch.empty(T, dtype=torch.int64, device="cuda")
