@@ -177,6 +177,8 @@ int ucg_reduce_cl_i64(const int64_t* const* elem_ptrs, uint64_t count, uint64_t 
  * bit-identical to the IEEE-double host test. seeds / samples: HOST arrays. */
 int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
                 void* stream);
+/* Class-D form for the seam-B executor: flags[gid] = hit(seed, gid) (device u8). */
+int ucg_pi_flags(uint64_t seed, uint64_t samples, uint8_t* flags, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* 3x3 Sobel on row bands (workload C4)                                       */

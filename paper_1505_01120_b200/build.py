@@ -120,8 +120,8 @@ def build_tests(force: bool = False, verbose: bool = False) -> Path | None:
     src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
     if not src.exists() or not (REF_INC / "ucores" / "engine.hpp").exists():
         return out if out.exists() else None
-    eng = build_engine(force=False, verbose=verbose)
-    deps = [src] + list((HOST / "ucores_b200").glob("*.hpp")) + [eng] if eng else [src]
+    cuda_lib = build_cuda(force=False, verbose=verbose)
+    deps = [src, cuda_lib] + list((HOST / "ucores_b200").glob("*.hpp")) + list(INCLUDE.glob("*.h"))
     if not (force or _stale(out, deps)):
         return out
     out.parent.mkdir(parents=True, exist_ok=True)

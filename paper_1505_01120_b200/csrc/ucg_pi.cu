@@ -87,10 +87,28 @@ __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTas
   }
 }
 
+// Class-D form of the same body (the seam-B contract of the pi kernel):
+// flags[gid] = hit(seed, gid) for gid in [0, samples).
+__global__ void __launch_bounds__(256) k_pi_flags(uint64_t seed, uint64_t samples, uint8_t* __restrict__ flags) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < samples; g += stride)
+    flags[g] = uint8_t(pi_hit(seed ^ (g * kGamma)));
+}
+
 }  // namespace
 }  // namespace ucg
 
 using namespace ucg;
+
+extern "C" int ucg_pi_flags(uint64_t seed, uint64_t samples, uint8_t* flags, void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!samples) return UCG_OK;
+  if (!flags) return fail(UCG_ERR_ARG, "flags is null");
+  const unsigned grid = unsigned(std::min<uint64_t>((samples + 255) / 256, uint64_t(sm_count()) * 16));
+  k_pi_flags<<<grid, 256, 0, as_stream(stream)>>>(seed, samples, flags);
+  UCG_LAUNCHED();
+  return UCG_OK;
+}
 
 extern "C" int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
                            void* stream) {

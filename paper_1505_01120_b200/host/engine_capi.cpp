@@ -1,0 +1,123 @@
+// engine_capi.cpp — C entry points of libucores_engine.so (include/ucores_engine.h):
+// the unmodified reference Engine driven through the B200 drop-in drivers.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ucores/dataset.hpp"
+#include "ucores/engine.hpp"
+#include "ucores/errors.hpp"
+#include "ucores_b200/device_ops.hpp"
+#include "ucores_b200/gpu_cluster_driver.hpp"
+#include "ucores_b200/kernels.hpp"
+#include "ucores_engine.h"
+
+namespace {
+
+thread_local std::string t_err;
+
+template <class Fn>
+int guarded(Fn fn) {
+  try {
+    fn();
+    return UCD_OK;
+  } catch (const ucores::JobFailed& e) {
+    t_err = e.what();
+    return UCD_ERR_JOB_FAILED;
+  } catch (const ucores::EmptyDataset& e) {
+    t_err = e.what();
+    return UCD_ERR_EMPTY;
+  } catch (const ucores::ArityMismatch& e) {
+    t_err = e.what();
+    return UCD_ERR_ARITY;
+  } catch (const ucores::UnknownKernel& e) {
+    t_err = e.what();
+    return UCD_ERR_UNKNOWN;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return UCD_ERR_OTHER;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ucd_last_error(void) { return t_err.c_str(); }
+
+int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts, float a, float b, int op, int gpus,
+                     int mode, float* y_out, float* partials_out, float* result_out, double* seconds_out) {
+  return guarded([&] {
+    using namespace ucores;
+    using namespace ucores_b200;
+    KernelRegistry reg;
+    DeviceOpRegistry ops;
+    WorkloadParams p;
+    p.a = a;
+    p.b = b;
+    register_workload(reg, ops, p);
+    GpuClusterDriver::Options opt;
+    opt.max_gpus = gpus;
+    opt.mode = mode == UCD_MODE_PER_TASK ? GpuClusterDriver::Mode::PerTask : GpuClusterDriver::Mode::Batched;
+    GpuClusterDriver drv(reg, ops, opt);
+    Engine eng(drv, reg);
+    const std::string pk = op == 1 ? "pmax" : "psum", rk = op == 1 ? "max2" : "sum2";
+
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<Partition> parts(nparts);
+    std::uint64_t off = 0;
+    for (std::uint64_t q = 0; q < nparts; ++q) {
+      parts[q].elements.push_back(Element::f32(std::vector<float>(x + off, x + off + part_lens[q])));
+      off += part_lens[q];
+    }
+    Dataset d(std::move(parts));
+    Dataset y = eng.map_cl(d, "axpb");
+    Dataset ps = eng.map_cl_partition(y, pk);
+    Element r = eng.reduce_cl(ps, rk);
+    auto t1 = std::chrono::steady_clock::now();
+    if (seconds_out) *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+    if (result_out) *result_out = r.as_f32()[0];
+    if (y_out) {
+      std::uint64_t o = 0;
+      for (const Element& e : y.collect()) {
+        auto v = e.as_f32();
+        std::memcpy(y_out + o, v.data(), v.size_bytes());
+        o += v.size();
+      }
+    }
+    if (partials_out) {
+      std::uint64_t q = 0;
+      for (const Element& e : ps.collect()) partials_out[q++] = e.as_f32()[0];
+    }
+  });
+}
+
+int ucd_pi(uint64_t samples, uint64_t tasks, uint64_t seed, int gpus, int64_t* hits_out, double* seconds_out) {
+  return guarded([&] {
+    using namespace ucores;
+    using namespace ucores_b200;
+    KernelRegistry reg;
+    DeviceOpRegistry ops;
+    register_workload(reg, ops);
+    GpuClusterDriver::Options opt;
+    opt.max_gpus = gpus;
+    GpuClusterDriver drv(reg, ops, opt);
+    Engine eng(drv, reg);
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<Element> es;
+    for (uint64_t t = 0; t < tasks; ++t) {
+      const uint64_t n = samples / tasks + (t < samples % tasks ? 1 : 0);
+      es.push_back(Element::i64({static_cast<std::int64_t>(seed + t), static_cast<std::int64_t>(n)}));
+    }
+    Dataset r = eng.map_cl(create_dataset(std::move(es), tasks), "pi");
+    std::int64_t h = 0;
+    for (const Element& e : r.collect()) h += e.as_i64()[0];
+    auto t1 = std::chrono::steady_clock::now();
+    if (hits_out) *hits_out = h;
+    if (seconds_out) *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+  });
+}
+
+}  // extern "C"

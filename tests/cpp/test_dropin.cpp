@@ -1,0 +1,308 @@
+// test_dropin.cpp — GPU parity of the C++ drop-in through the UNMODIFIED
+// reference Engine (ucores/engine.hpp). Every operator runs twice on the
+// same Dataset: once with a reference-style host driver (WorkerRuntime +
+// HostSequentialExecutor, the CPU path) and once with GpuClusterDriver
+// (seam A, batched) / GpuWorkerRuntime (seam B). Outputs must be equal under
+// Element::operator== (bitwise, element.hpp:108-126); matmul within a TF32
+// tolerance. Built by paper_1505_01120_b200/build.py; run by
+// tests/test_cpp_dropin.py on a GPU box.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "ucores/dataset.hpp"
+#include "ucores/device.hpp"
+#include "ucores/engine.hpp"
+#include "ucores/worker.hpp"
+#include "ucores_b200/cuda_executor.hpp"
+#include "ucores_b200/device_ops.hpp"
+#include "ucores_b200/gpu_cluster_driver.hpp"
+#include "ucores_b200/kernels.hpp"
+
+using namespace ucores;
+using namespace ucores_b200;
+
+namespace {
+
+int g_fail = 0, g_pass = 0;
+#define EXPECT(cond, what)                                              \
+  do {                                                                  \
+    if (cond) {                                                         \
+      ++g_pass;                                                         \
+    } else {                                                            \
+      ++g_fail;                                                         \
+      std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, what);         \
+    }                                                                   \
+  } while (0)
+
+float u01(std::uint64_t seed, std::uint64_t i) {
+  return static_cast<float>(kernels::mix64(seed + (i + 1) * kernels::kGamma) >> 40) * (1.0f / 16777216.0f);
+}
+
+// CPU reference driver: reference WorkerRuntime + host executor, in place.
+class HostDriver : public ClusterDriver {
+ public:
+  HostDriver(const KernelRegistry& reg) : rt_("cpu0", reg, ImplKind::STD, "HOST", dev()) {}
+  static DeviceDescriptor dev() {
+    DeviceDescriptor d;
+    d.device_id = "host-cpu-0";
+    d.device_type = ExecutionMode::CPU;
+    return d;
+  }
+  std::uint64_t new_job_id() override { return ++job_; }
+  std::vector<TaskResult> run_wave(std::vector<Task> tasks, int max_retries) override {
+    std::vector<TaskResult> out;
+    for (const Task& t : tasks) {
+      for (int a = 0;; ++a) {
+        Message m = rt_.execute(t);
+        if (auto* r = std::get_if<TaskResultMsg>(&m)) {
+          out.push_back(std::move(r->result));
+          break;
+        }
+        if (a >= max_retries) throw JobFailed("task failed: " + std::get<TaskErrorMsg>(m).detail);
+      }
+    }
+    std::sort(out.begin(), out.end(), [](auto& a, auto& b) { return a.task_id < b.task_id; });
+    return out;
+  }
+
+ private:
+  WorkerRuntime rt_;
+  std::uint64_t job_ = 0;
+};
+
+Dataset f32_dataset(const std::vector<std::vector<float>>& es, std::size_t parts) {
+  std::vector<Element> v;
+  for (auto& e : es) v.push_back(Element::f32(e));
+  return create_dataset(std::move(v), parts);
+}
+
+bool same(const Dataset& a, const Dataset& b) {
+  if (a.partition_count() != b.partition_count()) return false;
+  for (std::size_t p = 0; p < a.partition_count(); ++p)
+    if (a.partitions()[p].elements != b.partitions()[p].elements) return false;
+  return true;
+}
+
+struct Fixture {
+  KernelRegistry reg;
+  DeviceOpRegistry ops;
+  Fixture(std::size_t sobel_w = 48, std::size_t mat_n = 128) {
+    WorkloadParams p;
+    p.sobel_width = sobel_w;
+    p.matmul_n = mat_n;
+    register_workload(reg, ops, p);
+  }
+};
+
+template <class Fn>
+void run_case(const char* name, Fn fn) {
+  const int before = g_fail;
+  auto t0 = std::chrono::steady_clock::now();
+  try {
+    fn();
+  } catch (const std::exception& e) {
+    ++g_fail;
+    std::printf("FAIL %s: exception %s\n", name, e.what());
+  }
+  auto ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  std::printf("%s %s (%.1f ms)\n", g_fail == before ? "ok  " : "FAIL", name, ms);
+}
+
+}  // namespace
+
+int main() {
+  Fixture fx;
+  HostDriver host(fx.reg);
+  GpuClusterDriver gpu(fx.reg, fx.ops);
+  GpuClusterDriver::Options per_task;
+  per_task.mode = GpuClusterDriver::Mode::PerTask;
+  GpuClusterDriver gpu_b(fx.reg, fx.ops, per_task);
+  Engine eh(host, fx.reg), eg(gpu, fx.reg), eb(gpu_b, fx.reg);
+  std::printf("gpus: %zu\n", gpu.gpu_count());
+
+  // C1: 2^20 fp32 as 4 elements in 4 partitions; ragged variant too
+  run_case("c1 map_cl/map_cl_partition/reduce_cl sum+max (seam A and B)", [&] {
+    for (auto [n, elems, parts] : std::vector<std::tuple<std::size_t, std::size_t, std::size_t>>{
+             {1u << 20, 4, 4}, {100003, 13, 5}, {70001, 7, 3}}) {
+      std::vector<std::vector<float>> es(elems);
+      std::size_t pos = 0;
+      for (std::size_t k = 0; k < elems; ++k) {
+        es[k].resize(n / elems + (k < n % elems ? 1 : 0));
+        for (auto& v : es[k]) v = u01(12345, pos++);
+      }
+      Dataset x = f32_dataset(es, parts);
+      Dataset yh = eh.map_cl(x, "axpb"), yg = eg.map_cl(x, "axpb"), yb = eb.map_cl(x, "axpb");
+      EXPECT(same(yh, yg), "map_cl(axpb) seam A bitwise");
+      EXPECT(same(yh, yb), "map_cl(axpb) seam B bitwise");
+      for (const char* op : {"sum", "max"}) {
+        Dataset ph = eh.map_cl_partition(yh, std::string("p") + op);
+        Dataset pg = eg.map_cl_partition(yg, std::string("p") + op);
+        Dataset pb = eb.map_cl_partition(yb, std::string("p") + op);
+        EXPECT(same(ph, pg), "map_cl_partition seam A bitwise");
+        EXPECT(same(ph, pb), "map_cl_partition seam B bitwise");
+        Element rh = eh.reduce_cl(ph, std::string(op) + "2");
+        EXPECT(rh == eg.reduce_cl(pg, std::string(op) + "2"), "reduce_cl seam A bitwise");
+        EXPECT(rh == eb.reduce_cl(pb, std::string(op) + "2"), "reduce_cl seam B bitwise");
+        // reduce_cl directly over the mapped vectors (stage-1 folds + stage-2 tree)
+        if (std::string(op) == "sum") {
+          Dataset vh = f32_dataset({{1, 2, 3}, {4, 5, 6}, {7, 8, 9}, {10, 11, 12}, {0.5f, -0.5f, 1e30f}}, 2);
+          EXPECT(eh.reduce_cl(vh, "vectoradd") == eg.reduce_cl(vh, "vectoradd"), "reduce_cl vectors");
+        }
+      }
+    }
+  });
+
+  run_case("fig3 vectoradd [1,2,3]+[4,5,6]", [&] {
+    Element r = eg.reduce_cl(f32_dataset({{1, 2, 3}, {4, 5, 6}}, 1), "vectoradd");
+    auto v = r.as_f32();
+    EXPECT(v.size() == 3 && v[0] == 5 && v[1] == 7 && v[2] == 9, "[5,7,9]");
+  });
+
+  run_case("SPEC acceptance 2: vectoradd n=2^20 P=8 checksum", [&] {
+    const std::size_t len = 1u << 20, P = 8;
+    std::vector<std::vector<float>> es(P, std::vector<float>(len));
+    for (std::size_t k = 0; k < P; ++k)
+      for (std::size_t i = 0; i < len; ++i) es[k][i] = static_cast<float>((k * len + i) % 1000);
+    Dataset d = f32_dataset(es, P);
+    Element r = eg.reduce_cl(d, "vectoradd");
+    double cs = 0;
+    for (float v : r.as_f32()) cs += v;
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.3f", cs);
+    EXPECT(std::string(buf) == "4189990528.000", "checksum 4189990528.000");
+    EXPECT(r == eh.reduce_cl(d, "vectoradd"), "bitwise vs host");
+  });
+
+  run_case("SPEC acceptance 5: isum2 tree-reduce == left fold, tasks == count-1", [&] {
+    std::uint64_t s = 7;
+    for (int c = 0; c < 40; ++c) {
+      const std::size_t count = 1 + kernels::mix64(s++) % 40, parts = 1 + kernels::mix64(s++) % 16,
+                        len = 1 + kernels::mix64(s++) % 5;
+      std::vector<Element> es;
+      std::vector<std::uint64_t> fold(len, 0);
+      for (std::size_t i = 0; i < count; ++i) {
+        std::vector<std::int64_t> v(len);
+        for (std::size_t j = 0; j < len; ++j) {
+          v[j] = static_cast<std::int64_t>(kernels::mix64(s++));
+          fold[j] += static_cast<std::uint64_t>(v[j]);
+        }
+        es.push_back(Element::i64(v));
+      }
+      Dataset d = create_dataset(std::move(es), parts);
+      const std::uint64_t before = gpu.tasks_run();
+      Element r = eg.reduce_cl(d, "isum2");
+      bool ok = true;
+      for (std::size_t j = 0; j < len; ++j) ok &= static_cast<std::uint64_t>(r.as_i64()[j]) == fold[j];
+      EXPECT(ok, "isum equals left fold");
+      EXPECT(gpu.tasks_run() - before == count - 1, "REDUCE_PAIR tasks == count-1");
+    }
+  });
+
+  run_case("pi 4M/8/42 -> 3141371 (golden), seam A and B", [&] {
+    std::vector<Element> es;
+    for (int t = 0; t < 8; ++t) es.push_back(Element::i64({42 + t, 500000}));
+    Dataset d = create_dataset(std::move(es), 8);
+    std::int64_t hits = 0;
+    for (const Element& e : eg.map_cl(d, "pi").collect()) hits += e.as_i64()[0];
+    EXPECT(hits == 3141371, "hits == 3141371");
+    EXPECT(same(eb.map_cl(d, "pi"), eh.map_cl(d, "pi")), "seam B pi bitwise vs host");
+  });
+
+  run_case("sobel bands (W=48, 16-row bands)", [&] {
+    const std::size_t H = 50, W = 48, R = 16;
+    std::vector<std::uint8_t> img(H * W);
+    for (std::size_t i = 0; i < img.size(); ++i)
+      img[i] = static_cast<std::uint8_t>(kernels::mix64(7 + (i + 1) * kernels::kGamma) >> 56);
+    std::vector<Element> bands;
+    for (std::size_t r0 = 0; r0 < H; r0 += R) {
+      const std::size_t rr = std::min(R, H - r0);
+      std::vector<std::uint8_t> b((rr + 2) * W, 0);
+      for (std::size_t k = 0; k < rr + 2; ++k) {
+        const long src = static_cast<long>(r0 + k) - 1;
+        if (src >= 0 && src < static_cast<long>(H)) std::copy_n(img.data() + src * W, W, b.data() + k * W);
+      }
+      bands.push_back(Element::bytes(b));
+    }
+    Dataset d = create_dataset(std::move(bands), 4);
+    Dataset h = eh.map_cl_partition(d, "sobel");
+    EXPECT(same(h, eg.map_cl_partition(d, "sobel")), "seam A sobel bitwise");
+    EXPECT(same(h, eb.map_cl_partition(d, "sobel")), "seam B sobel bitwise");
+  });
+
+  run_case("errors: empty partition -> JobFailed, EmptyDataset, ArityMismatch, LengthMismatch", [&] {
+    bool jf = false;
+    try {
+      eg.map_cl_partition(f32_dataset({{1.0f}, {2.0f}}, 3), "psum");
+    } catch (const JobFailed&) {
+      jf = true;
+    }
+    EXPECT(jf, "empty partition JobFailed");
+    bool ed = false;
+    try {
+      eg.reduce_cl(Dataset(std::vector<Partition>(2)), "sum2");
+    } catch (const EmptyDataset&) {
+      ed = true;
+    }
+    EXPECT(ed, "EmptyDataset");
+    bool am = false;
+    try {
+      eg.map_cl(f32_dataset({{1.0f}}, 1), "sum2");
+    } catch (const ArityMismatch&) {
+      am = true;
+    }
+    EXPECT(am, "ArityMismatch");
+    bool lm = false;
+    try {
+      eg.reduce_cl(f32_dataset({{1.0f, 2.0f}, {1.0f}}, 1), "sum2");
+    } catch (const JobFailed&) {
+      lm = true;
+    }
+    EXPECT(lm, "LengthMismatch -> JobFailed");
+    const std::uint64_t before = gpu.tasks_run();
+    Element r = eg.reduce_cl(f32_dataset({{3.5f, 4.5f}}, 4), "sum2");
+    EXPECT(gpu.tasks_run() == before && r.as_f32()[0] == 3.5f, "single element: zero tasks");
+  });
+
+  run_case("no device body -> JobFailed (no CPU fallback)", [&] {
+    KernelRegistry reg;
+    DeviceOpRegistry ops;
+    reg.register_unary("hostonly", [] { return std::make_unique<kernels::Axpb>(1.f, 0.f); });
+    GpuClusterDriver d(reg, ops);
+    Engine e(d, reg);
+    bool jf = false;
+    try {
+      e.map_cl(f32_dataset({{1.0f}}, 1), "hostonly");
+    } catch (const JobFailed&) {
+      jf = true;
+    }
+    EXPECT(jf, "JobFailed");
+  });
+
+  run_case("C2-shaped map->psum->reduce at 2^27 (16 partitions of 2^23)", [&] {
+    const std::size_t P = 16, L = 1u << 23;
+    std::vector<std::vector<float>> es(P, std::vector<float>(L));
+    for (std::size_t p = 0; p < P; ++p)
+      for (std::size_t i = 0; i < L; ++i) es[p][i] = u01(1000 + p, i);
+    Dataset x = f32_dataset(es, P);
+    es.clear();
+    auto t0 = std::chrono::steady_clock::now();
+    Dataset yg = eg.map_cl(x, "axpb");
+    Element rg = eg.reduce_cl(eg.map_cl_partition(yg, "psum"), "sum2");
+    auto t1 = std::chrono::steady_clock::now();
+    Dataset yh = eh.map_cl(x, "axpb");
+    Element rh = eh.reduce_cl(eh.map_cl_partition(yh, "psum"), "sum2");
+    auto t2 = std::chrono::steady_clock::now();
+    EXPECT(same(yh, yg), "y bitwise");
+    EXPECT(rg == rh, "sum bitwise");
+    std::printf("  engine e2e: gpu %.1f ms, host-seq %.1f ms\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
+  });
+
+  std::printf("RESULT pass=%d fail=%d\n", g_pass, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}

@@ -294,3 +294,28 @@ def test_sobel_golden_and_random(cuda, golden):
         assert np.array_equal(got, want)
         if (H, W) == (g["H"], g["W"]):
             assert O.fnv64(got) == g["fnv"]
+
+
+# ---- the reference Engine through the C++ drop-in (libucores_engine.so) ------------
+
+@pytest.mark.parametrize("mode", ["batched", "per_task"])
+def test_engine_capi_pipeline(cuda, golden, mode):
+    from paper_1505_01120_b200 import engine_capi
+
+    g = golden["c2_small"]
+    P, L = g["P"], g["L"]
+    xs = [O.fill_uniform(1000 + p, L) for p in range(P)]
+    xs[P // 2][L // 3] = 1.5
+    for op in ("sum", "max"):
+        y, partials, r, _ = engine_capi.pipeline_f32(np.concatenate(xs), [L] * P, op=op, mode=mode)
+        assert O.fnv64(y) == g["y_fnv"]
+        assert [O.f32_bits(v) for v in partials] == g["partials_" + op]
+        assert O.f32_bits(r) == g["total_" + op]
+
+
+def test_engine_capi_pi(cuda, golden):
+    from paper_1505_01120_b200 import engine_capi
+
+    case = golden["pi"][0]
+    hits, _ = engine_capi.pi(case["samples"], case["tasks"], case["seed"])
+    assert hits == case["hits"]
