@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--part-len", type=int, default=1 << 24)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-engine-e2e", action="store_true")
     ap.add_argument("--cpu-sample-parts", type=int, default=4)
     return ap.parse_args()
 
@@ -288,6 +289,24 @@ def our_arm(args, world, rank, local):
     peak, peak_kind = load_peak()
     traffic = load_traffic("fused_pass1_bytes_per_launch" if not args.no_fuse else "unfused_bytes_per_step")
 
+    # ---- e2e through the unmodified reference ucores::Engine + GpuClusterDriver -------
+    engine_e2e = None
+    if world == 1 and not args.no_engine_e2e:
+        try:
+            import numpy as np
+
+            from paper_1505_01120_b200 import engine_capi
+
+            xs = np.concatenate([pipe.x[b:b + n].cpu().numpy() for b, n in zip(pipe.layout.begins, pipe.local_lens)])
+            _, _, r_eng, sec = engine_capi.pipeline_f32(xs, pipe.local_lens, op=args.op, want_y=False)
+            engine_e2e = {"value": n_total / sec, "unit": UNIT, "seconds": sec,
+                          "path": "ucores::Engine map_cl/map_cl_partition/reduce_cl + GpuClusterDriver (seam A), "
+                                  "host Elements in, Element out (Dataset construction timed)",
+                          "result_matches": bool(np.float32(r_eng) == np.float32(result))}
+            del xs
+        except Exception as e:  # reported, not hidden
+            engine_e2e = {"value": None, "error": str(e)[:300]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -317,6 +336,7 @@ def our_arm(args, world, rank, local):
                          "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": kern_ms,
                          "peak_kind": peak_kind, "frac_of_8TBs": achieved / 8000.0},
             "cpu_baseline": cpu,
+            "e2e_reference_api": engine_e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "result": result,
