@@ -9,7 +9,9 @@
 // WorkerRuntime::execute.
 #pragma once
 
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <string_view>
 #include <utility>
@@ -96,6 +98,30 @@ inline ucores::PlatformDescriptor gpu_platform() {
   p.arch = gpu_count() > 0 && ucg_device_info_get(0, &info) == UCG_OK ? std::string(info.name) : "NVIDIA";
   for (int i = 0; i < gpu_count(); ++i) p.devices.push_back(b200_descriptor(i));
   return p;
+}
+
+/// Process-wide Gpu for a descriptor "cuda:N" (what make_executor needs when
+/// patched, INTEGRATION.md seam B).
+inline std::shared_ptr<Gpu> gpu_for(const ucores::DeviceDescriptor& d) {
+  static std::mutex mu;
+  static std::map<int, std::shared_ptr<Gpu>> gpus;
+  int ordinal = 0;
+  if (d.device_id.rfind("cuda:", 0) == 0) ordinal = std::stoi(d.device_id.substr(5));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& g = gpus[ordinal];
+  if (!g) g = std::make_shared<Gpu>(ordinal);
+  return g;
+}
+
+/// Process-wide registry holding the device bodies of the workload kernels.
+inline const DeviceOpRegistry& default_device_ops() {
+  static const DeviceOpRegistry ops = [] {
+    ucores::KernelRegistry unused;
+    DeviceOpRegistry r;
+    register_workload(unused, r);
+    return r;
+  }();
+  return ops;
 }
 
 /// WorkerRuntime (worker.hpp:18-82) with the run phase on a B200: provision

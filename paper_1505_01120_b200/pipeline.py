@@ -45,6 +45,42 @@ def shard_range(num_partitions: int, world: int, rank: int) -> range:
     return range(lo, hi)
 
 
+def gather_index(num_partitions: int, world: int) -> tuple[int, list[int]]:
+    """Padded all-gather layout: each rank sends max_local slots; returns
+    (max_local, positions of partitions 0..P-1 in the gathered buffer)."""
+    max_local = max(len(shard_range(num_partitions, world, r)) for r in range(world))
+    idx = []
+    for r in range(world):
+        idx.extend(r * max(1, max_local) + k for k in range(len(shard_range(num_partitions, world, r))))
+    return max(1, max_local), idx
+
+
+def gather_partials(local, num_partitions: int, world: int, group=None, send_buf=None, gather_buf=None,
+                    index=None, out=None):
+    """The exchange step of a sharded reduce_cl: every rank contributes the
+    partials of its partition block and receives all P partials in partition
+    order (NCCL all-gather on GPUs, any torch.distributed backend works)."""
+    import torch.distributed as dist
+
+    max_local, idx = gather_index(num_partitions, world)
+    dev = local.device
+    if send_buf is None:
+        send_buf = torch.empty(max_local, dtype=local.dtype, device=dev)
+    if gather_buf is None:
+        gather_buf = torch.empty(world * max_local, dtype=local.dtype, device=dev)
+    if index is None:
+        index = torch.tensor(idx, dtype=torch.int64, device=dev)
+    if out is None:
+        out = torch.empty(num_partitions, dtype=local.dtype, device=dev)
+    n = local.numel()
+    send_buf.fill_(0)
+    if n:
+        send_buf[:n].copy_(local)
+    dist.all_gather_into_tensor(gather_buf, send_buf, group=group)
+    torch.index_select(gather_buf, 0, index, out=out)
+    return out
+
+
 @dataclass
 class Layout:
     """Segment layout of a set of partitions in one device buffer."""
@@ -84,13 +120,9 @@ class MapReducePipeline:
         self.segtab = capi.SegTab(self.layout.begins, self.local_lens)
         self.scratch = torch.empty(max(1, self.segtab.scratch_floats), dtype=torch.float32, device=dev)
         self.partials = torch.empty(max(1, len(self.local_lens)), dtype=torch.float32, device=dev)
-        self.max_local = max(len(shard_range(self.P, world, r)) for r in range(world))
-        self.gather_buf = torch.empty(world * max(1, self.max_local), dtype=torch.float32, device=dev)
-        self.send_buf = torch.empty(max(1, self.max_local), dtype=torch.float32, device=dev)
-        idx = []
-        for r in range(world):
-            rr = shard_range(self.P, world, r)
-            idx.extend(r * self.max_local + k for k in range(len(rr)))
+        self.max_local, idx = gather_index(self.P, world)
+        self.gather_buf = torch.empty(world * self.max_local, dtype=torch.float32, device=dev)
+        self.send_buf = torch.empty(self.max_local, dtype=torch.float32, device=dev)
         self.gather_index = torch.tensor(idx, dtype=torch.int64, device=dev)
         self.all_partials = torch.empty(max(1, self.P), dtype=torch.float32, device=dev)
         self.result = torch.empty(1, dtype=torch.float32, device=dev)
@@ -134,14 +166,9 @@ class MapReducePipeline:
         if self.world == 1:
             ops.tree_reduce(self.partials, self.P, self.op, self.result, stream=stream)
             return self.result
-        import torch.distributed as dist
-
         n = len(self.local_lens)
-        self.send_buf.fill_(0.0)
-        if n:
-            self.send_buf[:n].copy_(self.partials[:n])
-        dist.all_gather_into_tensor(self.gather_buf, self.send_buf, group=self.group)
-        torch.index_select(self.gather_buf, 0, self.gather_index, out=self.all_partials)
+        gather_partials(self.partials[:n], self.P, self.world, self.group, self.send_buf, self.gather_buf,
+                        self.gather_index, self.all_partials)
         ops.tree_reduce(self.all_partials, self.P, self.op, self.result, stream=stream)
         return self.result
 
