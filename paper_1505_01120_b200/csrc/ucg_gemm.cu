@@ -1,10 +1,228 @@
-// ucg_gemm.cu — dense matmul device op (workload C5). tcgen05 kernel pending.
+// ucg_gemm.cu — dense matmul device op (workload C5) on the 5th-generation
+// tensor cores: tcgen05.mma kind::tf32, fp32 accumulators in TMEM, operands
+// staged by TMA into 128-byte-swizzled shared memory.
+//
+// C = A * B, all n x n row-major fp32. A tile is K-major (rows of A are
+// contiguous in k); B is row-major [k][n], i.e. MN-major for the MMA, which
+// tcgen05 accepts for TF32 (instruction-descriptor b_major = 1).
+//
+// CTA tile 128 x 256, k-block 32, 4-stage TMA ring (48 KB / stage):
+//   warp 0 lane 0  TMA producer: A box {32 k, 128 m} + 8 B boxes {32 n, 32 k}
+//   warp 1 lane 0  MMA issuer: 4 x tcgen05.mma (M128 N256 K8) per k-block,
+//                  tcgen05.commit -> frees the stage when the MMAs have read it
+//   warps 0-3      epilogue: tcgen05.ld 32x32b (row = TMEM lane) -> global
+// Shared-memory canonical layouts (cute/atom/mma_traits_sm100.hpp):
+//   A  K-major SW128:  8 rows x 128 B atoms, SBO = 1024 B; k-step = +32 B
+//   B  MN-major SW128 with 32-byte atoms (SWIZZLE_128B_BASE32B, the only
+//      MN-major layout tf32 accepts; TMA swizzle 128B_ATOM_32B): rows of
+//      128 B (32 n) per k, 4-row groups, LBO = strip = 4096 B (n direction),
+//      SBO = 512 B (k direction); k-step of 8 = +1024 B
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
 #include "ucg_common.cuh"
+
+namespace ucg {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 32, STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 4;        // 16 KB
+constexpr uint32_t B_STRIP = BK * 128;           // 32 k-rows x 128 B = 4 KB
+constexpr uint32_t B_BYTES = (BN / 32) * B_STRIP;  // 32 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack
+constexpr uint32_t TMEM_COLS = 256;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+// layout: 2 = SWIZZLE_128B (16-byte granules), 1 = SWIZZLE_128B_BASE32B (32-byte granules)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo_bytes >> 4) & 0x3FFFu) << 16) |
+         (uint64_t((sbo_bytes >> 4) & 0x3FFFu) << 32) | (1ull << 46) /* version: sm100 */ |
+         (uint64_t(layout) << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, A K-major, B MN-major, N=256, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) | (uint32_t(BN >> 3) << 17) |
+                            (uint32_t(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1)
+    k_gemm_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, float* __restrict__ C,
+                int n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = n / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* a = smem + s * STAGE_BYTES;
+      uint8_t* b = a + A_BYTES;
+      mbar_expect_tx(&full[s], STAGE_BYTES);
+      tma_2d(a, &tmA, &full[s], kb * BK, m0);
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) tma_2d(b + j * B_STRIP, &tmB, &full[s], n0 + 32 * j, kb * BK);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer (single thread) ----
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t a = smem_addr(smem + s * STAGE_BYTES);
+      const uint32_t b = a + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 8; ++k) {
+        const uint64_t adesc = smem_desc(a + 32u * k, 16u, 1024u, 2u);
+        const uint64_t bdesc = smem_desc(b + 1024u * k, B_STRIP, 512u, 1u);
+        mma_tf32(tmem, adesc, bdesc, (kb | k) != 0);
+      }
+      mma_commit(&empty[s]);  // stage reusable once these MMAs have read it
+    }
+    mma_commit(&tfull);  // accumulator complete
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> registers -> global (row = TMEM lane) ----
+  mbar_wait(&tfull, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  float* crow = C + size_t(row) * n + n0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(c * 32);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float4* dst = reinterpret_cast<float4*>(crow + c * 32);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                           __uint_as_float(r[4 * q + 3]));
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+             uint32_t box_outer, CUtensorMapSwizzle swz) {
+  auto fn = encode_fn();
+  if (!fn) return fail(UCG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(UCG_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return UCG_OK;
+}
+
+}  // namespace
+}  // namespace ucg
 
 using namespace ucg;
 
 extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t n, void* stream) {
-  (void)A; (void)B; (void)C; (void)n; (void)stream;
   if (int rc = check_device()) return rc;
-  return fail(UCG_ERR_ARG, "ucg_gemm_tf32: not built in this revision");
+  if (!n) return UCG_OK;
+  if (!A || !B || !C) return fail(UCG_ERR_ARG, "null argument");
+  if (n % BN || n > (1u << 30)) return fail(UCG_ERR_ARG, "gemm: n must be a multiple of 256");
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return fail(UCG_ERR_ARG, "gemm: 16-byte alignment required");
+  CUtensorMap tmA, tmB;
+  if (int rc = make_map(&tmA, A, n, n, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;   // A[m][k]: inner k, box {32 k, 128 m}
+  if (int rc = make_map(&tmB, B, n, n, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return rc;   // B[k][n]: inner n, box {32 n, 32 k}
+  static bool attr = false;
+  if (!attr) {
+    UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr = true;
+  }
+  dim3 grid(unsigned(n / BN), unsigned(n / BM));
+  k_gemm_tf32<<<grid, 128, SMEM_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
+  UCG_LAUNCHED();
+  return UCG_OK;
 }

@@ -90,7 +90,7 @@ bool same(const Dataset& a, const Dataset& b) {
 struct Fixture {
   KernelRegistry reg;
   DeviceOpRegistry ops;
-  Fixture(std::size_t sobel_w = 48, std::size_t mat_n = 128) {
+  Fixture(std::size_t sobel_w = 48, std::size_t mat_n = 256) {
     WorkloadParams p;
     p.sobel_width = sobel_w;
     p.matmul_n = mat_n;
@@ -265,6 +265,28 @@ int main() {
     const std::uint64_t before = gpu.tasks_run();
     Element r = eg.reduce_cl(f32_dataset({{3.5f, 4.5f}}, 4), "sum2");
     EXPECT(gpu.tasks_run() == before && r.as_f32()[0] == 3.5f, "single element: zero tasks");
+  });
+
+  run_case("matmul n=256 (TF32 tcgen05 vs host fp32, tolerance), seam A and B", [&] {
+    const std::size_t n = 256;
+    std::vector<std::vector<float>> es(2, std::vector<float>(2 * n * n));
+    for (std::size_t e = 0; e < 2; ++e)
+      for (std::size_t i = 0; i < 2 * n * n; ++i) es[e][i] = 2.0f * u01(100 + e, i) - 1.0f;
+    Dataset d = f32_dataset(es, 2);
+    Dataset h = eh.map_cl(d, "matmul");
+    for (Engine* e : {&eg, &eb}) {
+      Dataset g = e->map_cl(d, "matmul");
+      for (std::size_t p = 0; p < 2; ++p) {
+        auto a = h.partitions()[p].elements[0].as_f32();
+        auto b = g.partitions()[p].elements[0].as_f32();
+        double ss = 0, md = 0;
+        for (std::size_t i = 0; i < a.size(); ++i) {
+          ss += double(a[i]) * a[i];
+          md = std::max(md, std::abs(double(a[i]) - b[i]));
+        }
+        EXPECT(md <= 1e-2 * std::sqrt(ss / a.size()), "matmul within TF32 tolerance");
+      }
+    }
   });
 
   run_case("no device body -> JobFailed (no CPU fallback)", [&] {

@@ -1,0 +1,64 @@
+"""C5 dense matmul on tcgen05 (kind::tf32, fp32 accumulate in TMEM): checked
+against an fp64 product of the same fp32 inputs. Tolerance (TF32 has a
+10-bit mantissa; the tensor core truncates the fp32 operands):
+rms(C - C64) / rms(C64) <= 1.5e-3 and max|C - C64| <= 1e-2 * rms(C64)."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _rand(n, seed, cuda):
+    from paper_1505_01120_b200 import ops
+
+    t = torch.empty(n * n, dtype=torch.float32, device=cuda)
+    ops.fill_uniform_(t, seed)
+    return (t * 2 - 1).view(n, n)
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048])
+def test_gemm_tf32_vs_fp64(cuda, n):
+    from paper_1505_01120_b200 import ops
+
+    A, B = _rand(n, 100, cuda), _rand(n, 101, cuda)
+    Cm = torch.full((n, n), float("nan"), device=cuda)
+    ops.gemm_tf32(A, B, Cm, n)
+    ref = A.double() @ B.double()
+    err = (Cm.double() - ref)
+    rms_ref = float(ref.pow(2).mean().sqrt())
+    assert torch.isfinite(Cm).all()
+    assert float(err.pow(2).mean().sqrt()) / rms_ref <= 1.5e-3
+    assert float(err.abs().max()) <= 1e-2 * rms_ref
+
+
+def test_gemm_matches_oracle_small(cuda, golden):
+    """The golden matmul case (n=24) zero-padded to 256: same fp32 inputs as the
+    reference harness; compared with the oracle's fp32 product (tolerance)."""
+    from paper_1505_01120_b200 import ops
+
+    g = golden["matmul"]
+    n0 = g["n"]
+    ab = (2.0 * O.fill_uniform(g["seed"], 2 * n0 * n0) - np.float32(1.0)).astype(np.float32)
+    A0, B0 = ab[: n0 * n0].reshape(n0, n0), ab[n0 * n0:].reshape(n0, n0)
+    C0 = O.matmul(A0, B0)
+    assert O.fnv64(C0) == g["c"]["fnv"]  # the oracle reproduces the reference exactly
+    n = 256
+    A = np.zeros((n, n), np.float32)
+    B = np.zeros((n, n), np.float32)
+    A[:n0, :n0], B[:n0, :n0] = A0, B0
+    Cm = torch.empty(n, n, device=cuda)
+    ops.gemm_tf32(torch.from_numpy(A).to(cuda), torch.from_numpy(B).to(cuda), Cm, n)
+    got = Cm.cpu().numpy()
+    assert np.abs(got[:n0, :n0] - C0).max() <= 1e-2 * np.sqrt((C0.astype(np.float64) ** 2).mean())
+    assert np.all(got[n0:, :] == 0) and np.all(got[:, n0:] == 0)
+
+
+def test_gemm_rejects_bad_sizes(cuda):
+    from paper_1505_01120_b200 import KernelPanic, ops
+
+    x = torch.zeros(100, 100, device=cuda)
+    with pytest.raises(KernelPanic):
+        ops.gemm_tf32(x, x, x, 100)
