@@ -79,11 +79,13 @@ struct ucg_segtab {
   uint64_t* d_first_item;  // [nseg+1]
   uint32_t* d_item_seg;    // [nitems]
   uint64_t max_items_per_seg;
+  int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
 };
 
 namespace ucg {
-// Work item = one aligned block of kItemFloats floats of one segment
-// (the last item of a segment may be partial).
-constexpr int kItemLog2 = 14;
-constexpr uint64_t kItemFloats = 1ull << kItemLog2;
+// Work item = one aligned block of 2^item_log2 floats of one segment (the
+// last item of a segment may be partial). The size is picked per segment
+// table in [2^11, 2^14] so the last wave of warps is nearly full.
+constexpr int kMinItemLog2 = 11;
+constexpr int kMaxItemLog2 = 14;
 }  // namespace ucg

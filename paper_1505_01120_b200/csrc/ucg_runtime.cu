@@ -251,11 +251,32 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if (int rc = check_device()) return rc;
   if (nseg && (!begin || !len)) return fail(UCG_ERR_ARG, "begin/len is null");
   if (nseg >= (1ull << 32)) return fail(UCG_ERR_ARG, "too many segments");
+  // work-item size: the largest 2^L (L in [11,14]) whose item count fills the
+  // last wave of resident warps to >= 95% (else the best-filled one)
+  uint64_t total = 0;
+  for (uint64_t s = 0; s < nseg; ++s) total += len[s];
+  const uint64_t warps = uint64_t(sm_count()) * 16;
+  int item_log2 = kMaxItemLog2;
+  double best = -1.0;
+  for (int L = kMaxItemLog2; L >= kMinItemLog2; --L) {
+    uint64_t items = 0;
+    for (uint64_t s = 0; s < nseg; ++s) items += (len[s] + (1ull << L) - 1) >> L;
+    const double fill = items ? double(items) / double((items + warps - 1) / warps * warps) : 1.0;
+    if (fill > best + 1e-9) {
+      best = fill;
+      item_log2 = L;
+    }
+    if (fill >= 0.95) {
+      item_log2 = L;
+      break;
+    }
+  }
+  (void)total;
   std::vector<uint64_t> first(nseg + 1, 0);
   uint64_t maxi = 0;
   for (uint64_t s = 0; s < nseg; ++s) {
     if (begin[s] % 4) return fail(UCG_ERR_ARG, "segment " + std::to_string(s) + " begin is not 16-byte aligned");
-    const uint64_t items = (len[s] + kItemFloats - 1) >> kItemLog2;
+    const uint64_t items = (len[s] + (1ull << item_log2) - 1) >> item_log2;
     first[s + 1] = first[s] + items;
     if (items > maxi) maxi = items;
   }
@@ -268,6 +289,7 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   t->nseg = nseg;
   t->nitems = nitems;
   t->max_items_per_seg = maxi;
+  t->item_log2 = item_log2;
   auto cleanup = [&](cudaError_t e, const char* what) {
     cudaFree(t->d_begin);
     cudaFree(t->d_len);

@@ -3,7 +3,9 @@
 // out(r,c) = min(255, |Gx|+|Gy|) over the band's halo'd input, zero outside
 // the image columns (oracle/ucores_oracle.c orc_sobel_band_u8). Separable
 // form: with dh(c) = p(c+1)-p(c-1) and sh(c) = p(c-1)+2p(c)+p(c+1) per row,
-// Gx = dh(r0)+2dh(r1)+dh(r2) and Gy = sh(r2)-sh(r0).
+// Gx = dh(r0)+2dh(r1)+dh(r2) and Gy = sh(r2)-sh(r0). Arithmetic is packed two
+// pixels per 32-bit register (biased 16-bit halves, byte permutes to build
+// the neighbour vectors, sm_100 packed 16x2 min/max), ~7 integer ops/pixel.
 //
 // Data movement: one thread owns 16 consecutive columns (one 128-bit load
 // per input row) and walks down a strip of kStrip output rows keeping the
@@ -32,32 +34,55 @@ struct SobelBands {
   uint32_t nbands;
 };
 
+// Row terms for 16 pixels as 8 packed pairs (pixel 2i in the low 16 bits,
+// pixel 2i+1 in the high 16 bits), biased so no half ever borrows:
+//   dh = p(c+1) - p(c-1) + 256   in [1, 511]
+//   sh = p(c-1) + 2p(c) + p(c+1) in [0, 1020]
 struct RowTerms {
-  int dh[16];
-  int sh[16];
+  uint32_t dh[8];
+  uint32_t sh[8];
 };
 
-// Load one input row segment (16 px at column c0) and build its dh/sh terms.
-__device__ __forceinline__ void load_row(const uint8_t* __restrict__ row, uint64_t width, uint64_t c0, int lane,
-                                         bool active, RowTerms& t) {
-  uint4 w = make_uint4(0, 0, 0, 0);
-  if (active) w = *reinterpret_cast<const uint4*>(row + c0);
-  // neighbour bytes: byte 15 of lane-1, byte 0 of lane+1 (edge lanes read directly)
-  uint32_t left = __shfl_up_sync(0xffffffffu, w.w, 1) >> 24;
-  uint32_t right = __shfl_down_sync(0xffffffffu, w.x, 1) & 0xffu;
-  if (lane == 0) left = (active && c0 > 0) ? row[c0 - 1] : 0u;
-  if (lane == 31 || !active) right = (active && c0 + 16 < width) ? row[c0 + 16] : 0u;
-  // a lane past the row end contributes zeros; the lane before it must see 0 too
-  int p[18];
-  p[0] = int(left);
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+// A fetched input row segment: the thread's 16 bytes plus, for the warp's
+// edge lanes, the neighbour byte outside the warp's 512-byte span.
+struct RawRow {
+  uint4 w;
+  uint32_t edge;
+};
+
+__device__ __forceinline__ RawRow fetch_row(const uint8_t* __restrict__ row, uint64_t width, uint64_t c0, int lane,
+                                            bool active, bool exists) {
+  RawRow q{make_uint4(0, 0, 0, 0), 0u};
+  if (exists && active) q.w = __ldcs(reinterpret_cast<const uint4*>(row + c0));
+  if (exists && active) {
+    if (lane == 0 && c0 > 0) q.edge = row[c0 - 1];
+    if (lane == 31 && c0 + 16 < width) q.edge = row[c0 + 16];
+  }
+  return q;
+}
+
+// Build the row terms from a fetched row (neighbour bytes by shuffle).
+__device__ __forceinline__ void make_terms(const RawRow& q, int lane, RowTerms& t) {
+  uint32_t left = __shfl_up_sync(0xffffffffu, q.w.w, 1) >> 24;
+  uint32_t right = __shfl_down_sync(0xffffffffu, q.w.x, 1) & 0xffu;
+  // a lane past the row end holds zeros, which is the out-of-image value
+  if (lane == 0) left = q.edge;
+  if (lane == 31) right = q.edge;
+  const uint32_t ws[6] = {left << 24, q.w.x, q.w.y, q.w.z, q.w.w, right};
 #pragma unroll
-  for (int i = 0; i < 16; ++i) p[i + 1] = int((ws[i >> 2] >> (8 * (i & 3))) & 0xffu);
-  p[17] = int(right);
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t cur = ws[k + 1];
+    const uint32_t sl = __byte_perm(ws[k], cur, 0x6543);      // p(4k-1) .. p(4k+2)
+    const uint32_t sr = __byte_perm(cur, ws[k + 2], 0x4321);  // p(4k+1) .. p(4k+4)
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    t.dh[i] = p[i + 2] - p[i];
-    t.sh[i] = p[i] + 2 * p[i + 1] + p[i + 2];
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t sel = h ? 0x4342u : 0x4140u;  // bytes (2h, 2h+1) -> 16-bit halves
+      const uint32_t E = __byte_perm(cur, 0, sel);
+      const uint32_t L = __byte_perm(sl, 0, sel);
+      const uint32_t R = __byte_perm(sr, 0, sel);
+      t.dh[2 * k + h] = R - L + 0x01000100u;
+      t.sh[2 * k + h] = L + R + (E << 1);
+    }
   }
 }
 
@@ -84,24 +109,56 @@ __global__ void __launch_bounds__(kSobelThreads)
     uint8_t* dst = out + bands.out_off[lo] + r0 * width;
     const uint64_t c0 = (wcol * 32 + lane) * 16;
     const bool active = c0 < width;
-    RowTerms a, b, c;
-    load_row(src, width, c0, lane, active, a);
-    load_row(src + width, width, c0, lane, active, b);
-    for (uint64_t r = 0; r < nrows; ++r) {
-      load_row(src + (r + 2) * width, width, c0, lane, active, c);
-      uint32_t o[4] = {0, 0, 0, 0};
+    // output row r from input rows (top, mid, bottom) = (r, r+1, r+2)
+    auto emit = [&](uint64_t r, const RowTerms& a, const RowTerms& b, const RowTerms& c) {
+      uint32_t o[8];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int gx = a.dh[i] + 2 * b.dh[i] + c.dh[i];
-        const int gy = c.sh[i] - a.sh[i];
-        const int m = min(255, abs(gx) + abs(gy));
-        o[i >> 2] |= uint32_t(m) << (8 * (i & 3));
+      for (int i = 0; i < 8; ++i) {
+        // per half: gx' = Gx + 1024, gy' = Gy + 1024, both in [4, 2044]
+        const uint32_t gx = a.dh[i] + c.dh[i] + (b.dh[i] << 1);
+        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;
+        // |G| + 1024 = max(g', 2048 - g') per half
+        const uint32_t ax = __vmaxu2(gx, 0x08000800u - gx);
+        const uint32_t ay = __vmaxu2(gy, 0x08000800u - gy);
+        // min(|Gx|+|Gy|, 255) + 2048 per half; its low byte is the output pixel
+        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);
       }
-      if (active) st_stream(reinterpret_cast<float4*>(dst + r * width + c0),
-                            make_float4(__uint_as_float(o[0]), __uint_as_float(o[1]), __uint_as_float(o[2]),
-                                        __uint_as_float(o[3])));
-      a = b;
-      b = c;
+      if (active) {
+        const uint32_t q0 = __byte_perm(o[0], o[1], 0x6420), q1 = __byte_perm(o[2], o[3], 0x6420);
+        const uint32_t q2 = __byte_perm(o[4], o[5], 0x6420), q3 = __byte_perm(o[6], o[7], 0x6420);
+        st_stream(reinterpret_cast<float4*>(dst + r * width + c0),
+                  make_float4(__uint_as_float(q0), __uint_as_float(q1), __uint_as_float(q2), __uint_as_float(q3)));
+      }
+    };
+    // 3-row register window rotated by unrolling (no copies); the raw loads of
+    // the next 3 input rows are issued before the current 3 are computed, so
+    // every warp keeps 3 x 512 B of loads in flight.
+    const uint64_t last_in = nrows + 1;  // input rows 0..nrows+1 exist for this strip
+    auto fetch = [&](uint64_t i) { return fetch_row(src + i * width, width, c0, lane, active, i <= last_in); };
+    RowTerms t0, t1, t2;
+    make_terms(fetch(0), lane, t0);
+    make_terms(fetch(1), lane, t1);
+    RawRow p0 = fetch(2), p1 = fetch(3), p2 = fetch(4);
+    uint64_t r = 0;
+    for (; r + 3 <= nrows; r += 3) {
+      const RawRow n0 = fetch(r + 5), n1 = fetch(r + 6), n2 = fetch(r + 7);
+      make_terms(p0, lane, t2);
+      emit(r, t0, t1, t2);
+      make_terms(p1, lane, t0);
+      emit(r + 1, t1, t2, t0);
+      make_terms(p2, lane, t1);
+      emit(r + 2, t2, t0, t1);
+      p0 = n0;
+      p1 = n1;
+      p2 = n2;
+    }
+    if (r < nrows) {
+      make_terms(p0, lane, t2);
+      emit(r, t0, t1, t2);
+      if (r + 1 < nrows) {
+        make_terms(p1, lane, t0);
+        emit(r + 1, t1, t2, t0);
+      }
     }
   }
 }

@@ -167,8 +167,14 @@ class MapReducePipeline:
             ops.tree_reduce(self.partials, self.P, self.op, self.result, stream=stream)
             return self.result
         n = len(self.local_lens)
-        gather_partials(self.partials[:n], self.P, self.world, self.group, self.send_buf, self.gather_buf,
-                        self.gather_index, self.all_partials)
+        if self.P % self.world == 0:
+            # equal blocks: the gathered buffer is already in partition order
+            import torch.distributed as dist
+
+            dist.all_gather_into_tensor(self.all_partials, self.partials[:n], group=self.group)
+        else:
+            gather_partials(self.partials[:n], self.P, self.world, self.group, self.send_buf, self.gather_buf,
+                            self.gather_index, self.all_partials)
         ops.tree_reduce(self.all_partials, self.P, self.op, self.result, stream=stream)
         return self.result
 
