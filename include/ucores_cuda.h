@@ -151,6 +151,33 @@ int ucg_segment_reduce_f32(const float* x, const ucg_segtab* t, int op, float* s
 int ucg_map_affine_segment_reduce_f32(const float* x, float* y, const ucg_segtab* t, float a,
                                       float b, int op, float* scratch, float* out, void* stream);
 
+/* Peer-exchange context for a reduce_cl over a collection sharded across
+ * GPUs, one process per GPU (replaces the ReducePair waves of stage 2 that
+ * combine partials living on different workers, engine.hpp:172-190). Each
+ * rank owns nloc consecutive partitions starting at part_offset of p_total.
+ * Setup: create -> export the IPC handle (ucg_xchg_handle_bytes bytes) ->
+ * exchange handles out of band (e.g. torch.distributed all_gather) -> open
+ * with all ranks' handles in rank order. */
+typedef struct ucg_xchg ucg_xchg;
+int ucg_xchg_create(int world, int rank, uint64_t nloc, uint64_t part_offset, uint64_t p_total, ucg_xchg** out);
+uint64_t ucg_xchg_handle_bytes(void);
+int ucg_xchg_export(const ucg_xchg* x, void* handle_out);
+int ucg_xchg_open(ucg_xchg* x, const void* all_handles);
+int ucg_xchg_error(const ucg_xchg* x, int* err_out); /* 1 if a peer never arrived (synchronous) */
+int ucg_xchg_destroy(ucg_xchg* x);
+
+/* mapCLPartition(psum|pmax) + reduceCL stage 2 in two launches: pass 1 over
+ * the work items (optionally fused with the axpb map when y != NULL: y is
+ * written), then one kernel that reduces each segment to `partials` and whose
+ * last CTA runs the pairing tree over all partitions into `result` (device,
+ * one float). With xchg != NULL that CTA first stores this rank's partials
+ * into every peer's buffer over NVLink and waits for all ranks' epoch flags,
+ * so every rank obtains the same, reference-ordered result with no separate
+ * collective launch. A segment table / exchange must not be used by two
+ * launches concurrently. */
+int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, float a, float b, int op,
+                              float* scratch, float* partials, ucg_xchg* xchg, float* result, void* stream);
+
 /* reduceCL stage 2 over n one-float partials in partition order: the pairing
  * tree with odd promotion (engine.hpp:172-190). out: one float (device). */
 int ucg_tree_reduce_f32(const float* x, uint64_t n, int op, float* out, void* stream);

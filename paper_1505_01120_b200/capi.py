@@ -68,6 +68,13 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_segment_reduce_f32": (i32, [vp, vp, C.c_int, vp, vp, vp]),
     "ucg_map_affine_segment_reduce_f32": (i32, [vp, vp, vp, f32, f32, C.c_int, vp, vp, vp]),
     "ucg_tree_reduce_f32": (i32, [vp, u64, C.c_int, vp, vp]),
+    "ucg_xchg_create": (i32, [C.c_int, C.c_int, u64, u64, u64, P(vp)]),
+    "ucg_xchg_handle_bytes": (u64, []),
+    "ucg_xchg_export": (i32, [vp, vp]),
+    "ucg_xchg_open": (i32, [vp, vp]),
+    "ucg_xchg_error": (i32, [vp, P(C.c_int)]),
+    "ucg_xchg_destroy": (i32, [vp]),
+    "ucg_segment_reduce_cl_f32": (i32, [vp, vp, vp, f32, f32, C.c_int, vp, vp, vp, vp, vp]),
     "ucg_reduce_cl_f32": (i32, [vp, u64, u64, P(u64), u64, C.c_int, vp, vp]),
     "ucg_reduce_cl_i64": (i32, [vp, u64, u64, P(u64), u64, vp, vp]),
     "ucg_pi_hits": (i32, [P(u64), P(u64), u64, vp, vp]),

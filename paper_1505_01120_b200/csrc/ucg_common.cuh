@@ -80,6 +80,21 @@ struct ucg_segtab {
   uint32_t* d_item_seg;    // [nitems]
   uint64_t max_items_per_seg;
   int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
+  uint32_t* d_done;        // finish-kernel CTA counter (zero between launches)
+};
+
+// Peer-exchange context of a sharded reduce_cl (one process per GPU).
+struct ucg_xchg {
+  int device;
+  int world, rank;
+  uint64_t nloc, part_offset, p_total;
+  uint64_t region_bytes, flags_offset;
+  uint8_t* region;          // this rank's IPC-exported buffer: [p_total floats | flags[world]]
+  uint64_t* d_peers;        // [world] device addresses of every rank's region (mapped)
+  uint8_t** peer_ptrs;      // host copy (opened IPC handles, own region at [rank])
+  uint32_t* d_err;
+  uint32_t epoch;
+  bool opened;
 };
 
 namespace ucg {

@@ -242,7 +242,7 @@ __device__ float cta_tree(const float* __restrict__ vals, uint64_t n, float* sm 
     int size = 1;
     while (uint64_t(size) < cnt) size <<= 1;
     for (int i = tid; i < size; i += kTreeThreads)
-      sm[i] = uint64_t(i) < cnt ? vals[base + i] : Op::identity();
+      sm[i] = uint64_t(i) < cnt ? __ldcg(vals + base + i) : Op::identity();
     __syncthreads();
     for (int w = size / 2; w >= 1; w >>= 1) {
       for (int i = tid; i < w; i += kTreeThreads) sm[i] = Op::apply(sm[2 * i], sm[2 * i + 1]);
@@ -290,6 +290,92 @@ __global__ void __launch_bounds__(kTreeThreads)
   }
   const float r = cta_tree<Op>(partial + f, n, sm, stk);
   if (threadIdx.x == 0) out[s] = r;
+}
+
+// ---- pass 2 + reduce_cl stage 2 (+ the cross-GPU exchange) in one kernel -------
+
+struct FinishArgs {
+  const float* partial;       // item roots from pass 1
+  const uint64_t* first_item;
+  uint64_t nseg;
+  float* out;                 // this rank's per-segment (partition) values
+  uint32_t* done;             // CTA-completion counter, reset by the last CTA
+  float* result;              // reduce_cl result (every rank gets it)
+  // sharded exchange (world > 1): region r = rank r's IPC-mapped buffer
+  int world, rank;
+  uint64_t part_offset;       // first global partition index of this rank
+  uint64_t p_total;           // P over all ranks
+  const uint64_t* peers;      // [world] region base addresses (this rank's own at [rank])
+  uint64_t flags_offset;      // byte offset of the [world] epoch flags inside a region
+  uint32_t epoch;
+  uint32_t* err;              // set to 1 when a peer never arrives
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One CTA per segment reduces that segment's item roots (pass 2). The last
+// CTA to finish then runs reduce_cl stage 2: on one GPU directly over the
+// partition values; sharded, it first stores this rank's values into every
+// peer's region over NVLink (P2P stores), raises its epoch flag there
+// (release, system scope), waits for all ranks' flags in its own region
+// (acquire) and runs the same pairing tree over all P values in partition
+// order — the collective fused into the reduction kernel, no NCCL launch.
+template <class Op>
+__global__ void __launch_bounds__(kTreeThreads) k_segment_finish(const __grid_constant__ FinishArgs p) {
+  __shared__ float sm[kTreeBlock];
+  __shared__ float stk[64];
+  __shared__ bool last;
+  const int tid = threadIdx.x;
+  const uint64_t s = blockIdx.x;
+  if (s < p.nseg) {
+    const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
+    const float r = n ? cta_tree<Op>(p.partial + f, n, sm, stk) : Op::empty();
+    if (tid == 0) __stcg(p.out + s, r);
+  }
+  if (!p.result) return;
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  if (tid == 0) *p.done = 0;
+  __threadfence();
+  const float* vals = p.out;
+  uint64_t nvals = p.nseg;
+  if (p.world > 1) {
+    for (int r = 0; r < p.world; ++r) {
+      float* g = reinterpret_cast<float*>(p.peers[r]) + p.part_offset;
+      for (uint64_t i = tid; i < p.nseg; i += blockDim.x) g[i] = __ldcg(p.out + i);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid < p.world) {
+      uint32_t* fl = reinterpret_cast<uint32_t*>(p.peers[tid] + p.flags_offset);
+      st_release_sys(fl + p.rank, p.epoch);
+      const uint32_t* mine = reinterpret_cast<const uint32_t*>(p.peers[p.rank] + p.flags_offset) + tid;
+      uint64_t spins = 0;
+      while (int32_t(ld_acquire_sys(mine) - p.epoch) < 0) {
+        __nanosleep(64);
+        if (++spins > (1ull << 24)) {  // ~1 s: a peer never arrived
+          atomicExch(p.err, 1u);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    vals = reinterpret_cast<const float*>(p.peers[p.rank]);
+    nvals = p.p_total;
+  }
+  const float root = nvals ? cta_tree<Op>(vals, nvals, sm, stk) : Op::empty();
+  if (tid == 0) *p.result = root;
 }
 
 template <class Op>
@@ -437,15 +523,26 @@ void dispatch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_t st)
 
 template <class Op>
 int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, float* out,
-                   cudaStream_t st) {
+                   float* result, ucg_xchg* xg, cudaStream_t st) {
   Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2, a, b, scratch};
   if (t->nitems) {
     if (y) dispatch_pass1<Op, true>(args, t, st);
     else dispatch_pass1<Op, false>(args, t, st);
     UCG_LAUNCHED();
   }
-  if (t->nseg) {
-    k_segment_pass2<Op><<<unsigned(t->nseg), kTreeThreads, 0, st>>>(scratch, t->d_first_item, out);
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr};
+  if (xg) {
+    f.world = xg->world;
+    f.rank = xg->rank;
+    f.part_offset = xg->part_offset;
+    f.p_total = xg->p_total;
+    f.peers = xg->d_peers;
+    f.flags_offset = xg->flags_offset;
+    f.epoch = ++xg->epoch;
+    f.err = xg->d_err;
+  }
+  if (t->nseg || result) {
+    k_segment_finish<Op><<<unsigned(std::max<uint64_t>(1, t->nseg)), kTreeThreads, 0, st>>>(f);
     UCG_LAUNCHED();
   }
   return UCG_OK;
@@ -531,8 +628,10 @@ int ucg_segment_reduce_f32(const float* x, const ucg_segtab* t, int op, float* s
   if (!t) return fail(UCG_ERR_ARG, "segment table is null");
   if (t->nseg && (!out || (t->nitems && (!x || !scratch)))) return fail(UCG_ERR_ARG, "null argument");
   if (t->nitems && !aligned16(x)) return fail(UCG_ERR_ARG, "x must be 16-byte aligned");
-  if (op == UCG_OP_SUM) return segment_reduce<OpSum>(x, nullptr, t, 0.f, 0.f, scratch, out, as_stream(stream));
-  if (op == UCG_OP_MAX) return segment_reduce<OpMax>(x, nullptr, t, 0.f, 0.f, scratch, out, as_stream(stream));
+  if (op == UCG_OP_SUM)
+    return segment_reduce<OpSum>(x, nullptr, t, 0.f, 0.f, scratch, out, nullptr, nullptr, as_stream(stream));
+  if (op == UCG_OP_MAX)
+    return segment_reduce<OpMax>(x, nullptr, t, 0.f, 0.f, scratch, out, nullptr, nullptr, as_stream(stream));
   return fail(UCG_ERR_ARG, "unknown op");
 }
 
@@ -542,8 +641,20 @@ int ucg_map_affine_segment_reduce_f32(const float* x, float* y, const ucg_segtab
   if (!t) return fail(UCG_ERR_ARG, "segment table is null");
   if (t->nseg && (!out || (t->nitems && (!x || !y || !scratch)))) return fail(UCG_ERR_ARG, "null argument");
   if (t->nitems && (!aligned16(x) || !aligned16(y))) return fail(UCG_ERR_ARG, "x/y must be 16-byte aligned");
-  if (op == UCG_OP_SUM) return segment_reduce<OpSum>(x, y, t, a, b, scratch, out, as_stream(stream));
-  if (op == UCG_OP_MAX) return segment_reduce<OpMax>(x, y, t, a, b, scratch, out, as_stream(stream));
+  if (op == UCG_OP_SUM) return segment_reduce<OpSum>(x, y, t, a, b, scratch, out, nullptr, nullptr, as_stream(stream));
+  if (op == UCG_OP_MAX) return segment_reduce<OpMax>(x, y, t, a, b, scratch, out, nullptr, nullptr, as_stream(stream));
+  return fail(UCG_ERR_ARG, "unknown op");
+}
+
+int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, float a, float b, int op,
+                              float* scratch, float* partials, ucg_xchg* xchg, float* result, void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!t || !result) return fail(UCG_ERR_ARG, "segment table / result is null");
+  if (t->nseg && (!partials || (t->nitems && (!x || !scratch)))) return fail(UCG_ERR_ARG, "null argument");
+  if (t->nitems && (!aligned16(x) || (y && !aligned16(y)))) return fail(UCG_ERR_ARG, "x/y must be 16-byte aligned");
+  if (xchg && (!xchg->opened || xchg->nloc != t->nseg)) return fail(UCG_ERR_ARG, "exchange not opened for this shard");
+  if (op == UCG_OP_SUM) return segment_reduce<OpSum>(x, y, t, a, b, scratch, partials, result, xchg, as_stream(stream));
+  if (op == UCG_OP_MAX) return segment_reduce<OpMax>(x, y, t, a, b, scratch, partials, result, xchg, as_stream(stream));
   return fail(UCG_ERR_ARG, "unknown op");
 }
 

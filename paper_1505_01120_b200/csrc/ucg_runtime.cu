@@ -295,6 +295,7 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
     cudaFree(t->d_len);
     cudaFree(t->d_first_item);
     cudaFree(t->d_item_seg);
+    cudaFree(t->d_done);
     delete t;
     return cuda_fail(e, what);
   };
@@ -303,6 +304,8 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if ((e = cudaMalloc(&t->d_len, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_first_item, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMalloc(&t->d_done, 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMemset(t->d_done, 0, 4)) != cudaSuccess) return cleanup(e, "cudaMemset");
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
@@ -320,7 +323,91 @@ int ucg_segtab_destroy(ucg_segtab* t) {
   cudaFree(t->d_len);
   cudaFree(t->d_first_item);
   cudaFree(t->d_item_seg);
+  cudaFree(t->d_done);
   delete t;
+  return UCG_OK;
+}
+
+// ---- peer exchange (sharded reduce_cl over NVLink) ------------------------------
+
+int ucg_xchg_create(int world, int rank, uint64_t nloc, uint64_t part_offset, uint64_t p_total, ucg_xchg** out) {
+  if (!out) return fail(UCG_ERR_ARG, "out is null");
+  *out = nullptr;
+  if (int rc = check_device()) return rc;
+  if (world < 1 || world > 64 || rank < 0 || rank >= world || part_offset + nloc > p_total)
+    return fail(UCG_ERR_ARG, "bad exchange geometry");
+  auto* x = new ucg_xchg{};
+  cudaGetDevice(&x->device);
+  x->world = world;
+  x->rank = rank;
+  x->nloc = nloc;
+  x->part_offset = part_offset;
+  x->p_total = p_total;
+  x->flags_offset = (p_total * 4 + 255) / 256 * 256;
+  x->region_bytes = x->flags_offset + 256;
+  x->peer_ptrs = new uint8_t*[world]();
+  cudaError_t e;
+  if ((e = cudaMalloc(&x->region, x->region_bytes)) != cudaSuccess || (e = cudaMemset(x->region, 0, x->region_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&x->d_peers, world * 8)) != cudaSuccess || (e = cudaMalloc(&x->d_err, 4)) != cudaSuccess ||
+      (e = cudaMemset(x->d_err, 0, 4)) != cudaSuccess) {
+    cudaFree(x->region);
+    cudaFree(x->d_peers);
+    cudaFree(x->d_err);
+    delete[] x->peer_ptrs;
+    delete x;
+    return cuda_fail(e, "ucg_xchg_create");
+  }
+  *out = x;
+  return UCG_OK;
+}
+
+uint64_t ucg_xchg_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int ucg_xchg_export(const ucg_xchg* x, void* handle_out) {
+  if (!x || !handle_out) return fail(UCG_ERR_ARG, "null argument");
+  cudaIpcMemHandle_t h;
+  UCG_CUDA(cudaIpcGetMemHandle(&h, x->region));
+  std::memcpy(handle_out, &h, sizeof h);
+  return UCG_OK;
+}
+
+int ucg_xchg_open(ucg_xchg* x, const void* all_handles) {
+  if (!x || !all_handles) return fail(UCG_ERR_ARG, "null argument");
+  if (x->opened) return UCG_OK;
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(all_handles);
+  std::vector<uint64_t> addrs(x->world);
+  for (int r = 0; r < x->world; ++r) {
+    if (r == x->rank) {
+      x->peer_ptrs[r] = x->region;
+    } else {
+      void* p = nullptr;
+      UCG_CUDA(cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess));
+      x->peer_ptrs[r] = static_cast<uint8_t*>(p);
+    }
+    addrs[r] = reinterpret_cast<uint64_t>(x->peer_ptrs[r]);
+  }
+  UCG_CUDA(cudaMemcpy(x->d_peers, addrs.data(), x->world * 8, cudaMemcpyHostToDevice));
+  x->opened = true;
+  return UCG_OK;
+}
+
+int ucg_xchg_error(const ucg_xchg* x, int* err_out) {
+  if (!x || !err_out) return fail(UCG_ERR_ARG, "null argument");
+  uint32_t e = 0;
+  UCG_CUDA(cudaMemcpy(&e, x->d_err, 4, cudaMemcpyDeviceToHost));
+  *err_out = int(e);
+  return UCG_OK;
+}
+
+int ucg_xchg_destroy(ucg_xchg* x) {
+  if (!x) return UCG_OK;
+  for (int r = 0; r < x->world; ++r)
+    if (x->peer_ptrs[r] && r != x->rank) cudaIpcCloseMemHandle(x->peer_ptrs[r]);
+  cudaFree(x->region);
+  cudaFree(x->d_peers);
+  cudaFree(x->d_err);
+  delete[] x->peer_ptrs;
+  delete x;
   return UCG_OK;
 }
 

@@ -9,9 +9,12 @@ Reference semantics (ucores/engine.hpp):
 Layout in HBM: every partition's concatenated payload is one segment starting
 at a 256-byte aligned float offset of one buffer (x and y share the layout).
 Sharding (SURVEY.md §8(e)): rank g of G holds partitions [gP/G, (g+1)P/G);
-the only exchange is an all-gather of the per-partition partials (NCCL via
-torch.distributed), after which every rank runs the reference stage-2 tree
-over all P partials in partition order — bit-identical to one GPU.
+the only exchange is of the per-partition partials, after which every rank
+runs the reference stage-2 tree over all P partials in partition order —
+bit-identical to one GPU. Default exchange "p2p": the finish kernel itself
+stores this rank's partials into every peer's buffer over NVLink (CUDA IPC
+mapped) and waits on epoch flags, so a step is two launches with no
+collective; "nccl" uses torch.distributed all-gather + a tree launch.
 
 With fused=True the map and the partition reduction run as ONE kernel (read
 x, write y, reduce y: 8 B/elem instead of 12); y is still materialised, so
@@ -103,8 +106,12 @@ class MapReducePipeline:
 
     def __init__(self, part_lens: list[int], a: float = 2.0, b: float = 1.0, op: str = "sum",
                  fused: bool = True, world: int = 1, rank: int = 0, device: torch.device | None = None,
-                 seed_base: int = 1000, plant_max: bool = True, group=None):
+                 seed_base: int = 1000, plant_max: bool = True, group=None, exchange: str = "p2p"):
+        """exchange: how a sharded reduce_cl combines partials — "p2p" (the
+        finish kernel stores into peers' buffers over NVLink and waits on
+        epoch flags; no collective launch) or "nccl" (all-gather + tree)."""
         self.P = len(part_lens)
+        self.exchange = exchange
         self.part_lens = list(part_lens)
         self.a, self.b, self.op, self.fused = float(a), float(b), op, fused
         self.world, self.rank, self.group = world, rank, group
@@ -178,9 +185,49 @@ class MapReducePipeline:
         ops.tree_reduce(self.all_partials, self.P, self.op, self.result, stream=stream)
         return self.result
 
+    def _setup_xchg(self) -> None:
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        h = C.c_void_p()
+        capi.call("ucg_xchg_create", self.world, self.rank, len(self.local_lens), self.owned.start, self.P,
+                  C.byref(h), phase="map_parameters")
+        self.xchg = h.value
+        nbytes = int(capi.load().ucg_xchg_handle_bytes())
+        mine = (C.c_char * nbytes)()
+        capi.call("ucg_xchg_export", self.xchg, mine)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(mine), group=self.group)
+        allh = (C.c_char * (nbytes * self.world)).from_buffer_copy(b"".join(handles))
+        capi.call("ucg_xchg_open", self.xchg, allh)
+
     def step(self) -> torch.Tensor:
-        self.map_and_partials()
-        return self.combine()
+        """One pass: map + partition reduce + reduce_cl (+ exchange when sharded)."""
+        if self.world > 1 and self.exchange == "nccl":
+            self.map_and_partials()
+            return self.combine()
+        if self.world > 1 and getattr(self, "xchg", None) is None:
+            self._setup_xchg()
+        xg = getattr(self, "xchg", None) if self.world > 1 else None
+        if self.fused:
+            ops.segment_reduce_cl(self.x, self.y, self.segtab, self.a, self.b, self.op, self.scratch, self.partials,
+                                  xg, self.result)
+        else:
+            ops.map_affine(self.x, self.y, self.a, self.b)
+            ops.segment_reduce_cl(self.y, None, self.segtab, self.a, self.b, self.op, self.scratch, self.partials,
+                                  xg, self.result)
+        return self.result
+
+    def exchange_error(self) -> int:
+        """1 if a peer never published its partials (checked synchronously)."""
+        import ctypes as C
+
+        if getattr(self, "xchg", None) is None:
+            return 0
+        e = C.c_int(0)
+        capi.call("ucg_xchg_error", self.xchg, C.byref(e))
+        return e.value
 
     # -- end to end: inputs from pinned host memory, result back to the host ------
     def setup_host_input(self, chunks: int = 8) -> None:
@@ -226,6 +273,9 @@ class MapReducePipeline:
         return float(self.host_result[0])
 
     def close(self) -> None:
+        if getattr(self, "xchg", None):
+            capi.load().ucg_xchg_destroy(self.xchg)
+            self.xchg = None
         self.segtab.close()
         for g in getattr(self, "groups", []):
             g[4].close()

@@ -1,0 +1,52 @@
+"""torchrun worker for tests/test_multigpu.py: a sharded C2-shaped pipeline on
+N GPUs must give bit-identical partials/results to the single-GPU oracle, with
+both exchanges (fused NVLink P2P in the finish kernel, and NCCL all-gather)."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import oracle_lib as O  # noqa: E402
+from paper_1505_01120_b200.pipeline import MapReducePipeline, partition_sizes  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    report = {"rank": rank, "ok": True, "cases": []}
+    for (P, total, op, fused, exchange) in [(8, 1 << 20, "sum", True, "p2p"), (7, 300001, "max", True, "p2p"),
+                                            (64, 1 << 22, "sum", False, "p2p"), (5, 100000, "sum", True, "nccl"),
+                                            (3, 50000, "max", False, "nccl")]:
+        lens = partition_sizes(total, P)
+        pipe = MapReducePipeline(lens, op=op, fused=fused, world=world, rank=rank, exchange=exchange)
+        for _ in range(3):  # repeated steps exercise the epoch flags
+            r = float(pipe.step().item())
+        partials = [O.tree_reduce(O.map_affine(O.fill_uniform(1000 + p, lens[p]), 2.0, 1.0)
+                                  if not (p == P // 2) else _planted(p, lens[p]), op) for p in range(P)]
+        want = O.tree_reduce(np.array(partials, np.float32), op)
+        got_local = pipe.partials.cpu().numpy()[:len(pipe.local_lens)]
+        ok_local = [O.f32_bits(got_local[k]) == O.f32_bits(partials[p]) for k, p in enumerate(pipe.owned)]
+        ok = all(ok_local) and O.f32_bits(np.float32(r)) == O.f32_bits(want) and pipe.exchange_error() == 0
+        report["cases"].append({"P": P, "op": op, "exchange": exchange, "ok": ok, "got": r, "want": float(want)})
+        report["ok"] &= ok
+        pipe.close()
+    print("MULTIGPU " + json.dumps(report), flush=True)
+    dist.destroy_process_group()
+    return 0 if report["ok"] else 1
+
+
+def _planted(p, n):
+    x = O.fill_uniform(1000 + p, n)
+    x[n // 3] = 1.5
+    return O.map_affine(x, 2.0, 1.0)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
