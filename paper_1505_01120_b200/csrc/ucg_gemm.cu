@@ -21,7 +21,9 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "ucg_common.cuh"
@@ -174,6 +176,141 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+// ---- persistent, warp-specialised variant ---------------------------------------
+// One CTA per SM loops over output tiles (grouped raster: 16 m-blocks per
+// n-block sweep so concurrently running CTAs share A and B in L2). TMEM holds
+// TWO 128x256 fp32 accumulators (all 512 columns): the MMA warp fills one while
+// the 4 epilogue warps drain the other, so tensor cores never wait for stores.
+//   warp 0 lane 0  TMA producer (smem ring continues across tiles)
+//   warp 1         TMEM allocator; lane 0 issues MMAs + commits
+//   warps 2-5      epilogue; warp w reads TMEM lanes 32*(w%4)..+31
+constexpr int kGroupM = 16;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& m0, int& n0) {
+  const int per_group = kGroupM * tiles_n;
+  const int g = t / per_group, idx = t % per_group;
+  const int gm = min(kGroupM, tiles_m - g * kGroupM);
+  m0 = (g * kGroupM + idx % gm) * BM;
+  n0 = (idx / gm) * BN;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_tf32_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           float* __restrict__ C, int n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = n / BM, tiles_n = n / BN, ntiles = tiles_m * tiles_n, nk = n / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0;
+        tile_coords(t, tiles_m, tiles_n, m0, n0);
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = int(q % STAGES);
+          if (q >= uint32_t(STAGES)) mbar_wait(&empty[s], ((q / STAGES) & 1) ^ 1);
+          uint8_t* a = smem + s * STAGE_BYTES;
+          uint8_t* b = a + A_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_2d(a, &tmA, &full[s], kb * BK, m0);
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) tma_2d(b + j * B_STRIP, &tmB, &full[s], n0 + 32 * j, kb * BK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t q = 0, i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const uint32_t acc = i & 1;
+        if (i >= 2) mbar_wait(&tempty[acc], ((i / 2) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * uint32_t(BN);
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = int(q % STAGES);
+          mbar_wait(&full[s], (q / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a = smem_addr(smem + s * STAGE_BYTES);
+          const uint32_t b = a + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t adesc = smem_desc(a + 32u * k, 16u, 1024u, 2u);
+            const uint64_t bdesc = smem_desc(b + 1024u * k, B_STRIP, 512u, 1u);
+            mma_tf32(d, adesc, bdesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int lg = warp & 3;  // TMEM lane group this warp may access
+    uint32_t i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      int m0, n0;
+      tile_coords(t, tiles_m, tiles_n, m0, n0);
+      const uint32_t acc = i & 1;
+      mbar_wait(&tfull[acc], (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float* crow = C + size_t(m0 + lg * 32 + lane) * n + n0;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + (uint32_t(lg * 32) << 16) + acc * uint32_t(BN) + uint32_t(c * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+              "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float4* dst = reinterpret_cast<float4*>(crow + c * 32);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          __stcs(dst + qq, make_float4(__uint_as_float(r[4 * qq]), __uint_as_float(r[4 * qq + 1]),
+                                       __uint_as_float(r[4 * qq + 2]), __uint_as_float(r[4 * qq + 3])));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -216,13 +353,24 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   CUtensorMap tmA, tmB;
   if (int rc = make_map(&tmA, A, n, n, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B)) return rc;   // A[m][k]: inner k, box {32 k, 128 m}
   if (int rc = make_map(&tmB, B, n, n, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return rc;   // B[k][n]: inner n, box {32 n, 32 k}
+  static const int variant = [] {
+    const char* e = getenv("UCG_GEMM_VARIANT");
+    return e ? atoi(e) : 1;
+  }();
   static bool attr = false;
   if (!attr) {
     UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr = true;
   }
-  dim3 grid(unsigned(n / BN), unsigned(n / BM));
-  k_gemm_tf32<<<grid, 128, SMEM_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
+  if (variant == 0) {
+    dim3 grid(unsigned(n / BN), unsigned(n / BM));
+    k_gemm_tf32<<<grid, 128, SMEM_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
+  } else {
+    const uint64_t ntiles = (n / BM) * (n / BN);
+    const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count())));
+    k_gemm_tf32_persistent<<<grid, 192, SMEM_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
+  }
   UCG_LAUNCHED();
   return UCG_OK;
 }

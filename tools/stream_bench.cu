@@ -136,6 +136,45 @@ __global__ void __launch_bounds__(256, 1) k_tma(const float* __restrict__ x, flo
   __syncthreads();
 }
 
+// per-warp TMA ring: lane 0 keeps S bulk copies of 4 KB chunks in flight for
+// its warp's contiguous items; all lanes read the chunk from smem, map, STG.
+template <int S>
+__global__ void __launch_bounds__(256) k_warp_tma(const float* __restrict__ x, float* __restrict__ y, uint64_t nitems,
+                                                  float a, float b) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[8][S];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* ring = reinterpret_cast<float*>(smem) + warp * S * 1024;
+  const uint64_t gw = uint64_t(blockIdx.x) * 8 + warp, nw = uint64_t(gridDim.x) * 8;
+  const uint64_t my_items = nitems > gw ? (nitems - gw + nw - 1) / nw : 0;
+  const uint64_t total = my_items * 16;  // 16 chunks of 1024 floats per 16K item
+  auto chunk_src = [&](uint64_t q) { return x + ((gw + (q >> 4) * nw) << 14) + ((q & 15) << 10); };
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint64_t q = 0; q < S && q < total; ++q) {
+      mbar_expect_tx(&bars[warp][q], 4096);
+      bulk_g2s(ring + q * 1024, chunk_src(q), 4096, &bars[warp][q]);
+    }
+  }
+  __syncwarp();
+  for (uint64_t q = 0; q < total; ++q) {
+    const int s = int(q % S);
+    mbar_wait(&bars[warp][s], uint32_t((q / S) & 1));
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = reinterpret_cast<const float4*>(ring + s * 1024)[u * 32 + lane];
+    __syncwarp();
+    if (lane == 0 && q + S < total) {
+      mbar_expect_tx(&bars[warp][s], 4096);
+      bulk_g2s(ring + s * 1024, chunk_src(q + S), 4096, &bars[warp][s]);
+    }
+    float* dst = y + (chunk_src(q) - x);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) __stcs(reinterpret_cast<float4*>(dst) + u * 32 + lane, aff4(v[u], a, b));
+  }
+}
+
 int main() {
   const uint64_t n = 1ull << 30;
   float *x, *y;
@@ -206,6 +245,23 @@ int main() {
     auto kf = k_tma<T, S, O>;
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (S + O) * T));
     bench("tma 8K x8 stages out4, 2 CTA/SM", [&] { kf<<<sms * 2, 256, (S + O) * T>>>(x, y, n * 4 / T, 2.f, 1.f); });
+  }
+  for (int S : {3, 4, 6}) {
+    for (int cps : {1, 2}) {
+      const int smem = 8 * S * 4096;
+      char nm[128];
+      snprintf(nm, sizeof nm, "warp-tma ring S=%d, %d CTA/SM (8 warps)", S, cps);
+      if (S == 3) {
+        CK(cudaFuncSetAttribute(k_warp_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bench(nm, [&] { k_warp_tma<3><<<sms * cps, 256, smem>>>(x, y, n >> 14, 2.f, 1.f); });
+      } else if (S == 4) {
+        CK(cudaFuncSetAttribute(k_warp_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bench(nm, [&] { k_warp_tma<4><<<sms * cps, 256, smem>>>(x, y, n >> 14, 2.f, 1.f); });
+      } else if (cps == 1) {
+        CK(cudaFuncSetAttribute(k_warp_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        bench(nm, [&] { k_warp_tma<6><<<sms * cps, 256, smem>>>(x, y, n >> 14, 2.f, 1.f); });
+      }
+    }
   }
   // correctness spot check of the last run
   std::vector<float> hx(8), hy(8);
