@@ -222,6 +222,15 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out,
                        uint64_t width, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* WordCount word-start flags                */
+/* ------------------------------------------------------------------------ */
+
+/* The wordcount kernel's run() over one chunk: flags[gid] = 1 iff bytes[gid]
+ * is a word character and (gid == 0 or bytes[gid-1] is a delimiter: space,
+ * tab, LF, CR — ucores/dataset.hpp:87-89), else 0. Device u8 arrays. */
+int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* flags, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* dense matmul (workload C5): tcgen05 tensor cores                           */
 /* ------------------------------------------------------------------------ */
 

@@ -25,6 +25,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <map>
 #include <iostream>
 #include <memory>
 #include <string>
@@ -294,6 +296,79 @@ class Matmul : public UnaryKernel {
   std::span<float> ab_, c_;
 };
 
+// WordCount: flags of word starts in run(), tokens counted
+// in map_return_value (keys in first-occurrence order); below the threshold
+// the host tokenises directly.
+class WordCount : public UnaryKernel {
+ public:
+  static bool delim(std::uint8_t b) { return b == ' ' || b == '\t' || b == '\n' || b == '\r'; }
+  explicit WordCount(std::uint64_t min_bytes) : min_(min_bytes) {}
+  void map_parameters(KernelContext& ctx, const Element& in) override {
+    b_ = in.as_bytes();
+    ctx.set_range(b_.size());
+    if (b_.size() < min_) {
+      ctx.set_device_execution(false);
+      return;
+    }
+    f_ = ctx.alloc<std::uint8_t>("flags", b_.size());
+  }
+  void run(KernelContext&, std::size_t g) override {
+    f_[g] = static_cast<std::uint8_t>(!delim(b_[g]) && (g == 0 || delim(b_[g - 1])));
+  }
+  Element map_return_value(KernelContext& ctx, const Element&) override {
+    Element::Table t;
+    std::map<std::string, std::size_t> idx;
+    auto add = [&](std::size_t s, std::size_t e) {
+      std::string k(reinterpret_cast<const char*>(b_.data()) + s, e - s);
+      auto it = idx.find(k);
+      if (it == idx.end()) {
+        idx.emplace(k, t.size());
+        t.emplace_back(k, 1);
+      } else {
+        t[it->second].second++;
+      }
+    };
+    const std::size_t n = b_.size();
+    if (ctx.device_execution()) {
+      auto f = ctx.take<std::uint8_t>("flags");
+      for (std::size_t i = 0; i < n; ++i) {
+        if (!f[i]) continue;
+        std::size_t e = i;
+        while (e < n && !delim(b_[e])) ++e;
+        add(i, e);
+        i = e;
+      }
+    } else {
+      for (std::size_t i = 0; i < n;) {
+        while (i < n && delim(b_[i])) ++i;
+        std::size_t e = i;
+        while (e < n && !delim(b_[e])) ++e;
+        if (e > i) add(i, e);
+        i = e;
+      }
+    }
+    return Element::table(std::move(t));
+  }
+
+ private:
+  std::uint64_t min_;
+  std::span<const std::uint8_t> b_;
+  std::span<std::uint8_t> f_;
+};
+
+// Synthetic corpus shared with tests/oracle_lib.py: word i = "w<mix64(seed+i)%97>",
+// followed by 1-2 copies of one delimiter chosen from " \t\n\r".
+std::string make_corpus(std::uint64_t seed, std::size_t words) {
+  std::string s;
+  const char dl[4] = {' ', '\t', '\n', '\r'};
+  for (std::size_t i = 0; i < words; ++i) {
+    const std::uint64_t z = mix64(seed + i);
+    s += "w" + std::to_string(z % 97);
+    s.append(1 + ((z >> 40) & 1), dl[(z >> 32) & 3]);
+  }
+  return s;
+}
+
 KernelRegistry make_registry(std::size_t sobel_width, std::size_t matmul_n) {
   KernelRegistry reg;
   reg.register_unary("axpb", [] { return std::make_unique<Axpb>(2.0f, 1.0f); });
@@ -306,6 +381,8 @@ KernelRegistry make_registry(std::size_t sobel_width, std::size_t matmul_n) {
   reg.register_unary("pi", [] { return std::make_unique<Pi>(); });
   reg.register_unary("sobel", [sobel_width] { return std::make_unique<Sobel>(sobel_width); });
   reg.register_unary("matmul", [matmul_n] { return std::make_unique<Matmul>(matmul_n); });
+  reg.register_unary("wordcount", [] { return std::make_unique<WordCount>(0); });
+  reg.register_unary("wordcount_host", [] { return std::make_unique<WordCount>(~0ull); });
   return reg;
 }
 
@@ -596,6 +673,55 @@ json run_golden() {
     Dataset r = eng.map_cl(d, "matmul");
     g["matmul"] = {{"n", n}, {"seed", 100}, {"c", element_json(r.collect()[0])}};
   }
+  // WordCount: "a b a" and a corpus ingested by the
+  // reference's own create_from_text chunker (dataset.hpp:94-139).
+  {
+    auto table_json = [](const Element& e) {
+      json t = json::array();
+      for (const auto& [k, c] : e.as_table()) t.push_back({k, c});
+      return t;
+    };
+    Dataset d1 = create_dataset({Element::bytes(std::string("a b a"))}, 1);
+    json w;
+    w["simple"] = table_json(eng.map_cl(d1, "wordcount").collect()[0]);
+    const std::string corpus = make_corpus(5, 30000);
+    const std::string path = "/tmp/ucores_wc_corpus.txt";
+    {
+      std::ofstream f(path, std::ios::binary);
+      f << corpus;
+    }
+    Dataset d = create_from_text(path, 16384);
+    Dataset dev = eng.map_cl(d, "wordcount");
+    Dataset host = eng.map_cl(d, "wordcount_host");
+    std::map<std::string, std::uint64_t> merged;
+    bool same = true;
+    std::vector<std::string> chunk_fnv;
+    const std::vector<Element> dev_e = dev.collect(), host_e = host.collect();
+    for (std::size_t i = 0; i < dev_e.size(); ++i) {
+      const Element& a = dev_e[i];
+      same &= a == host_e[i];
+      std::string ser;
+      for (const auto& [k, c] : a.as_table()) {
+        merged[k] += c;
+        ser += k + "\t" + std::to_string(c) + "\n";
+      }
+      chunk_fnv.push_back(hex64(fnv64(ser.data(), ser.size())));
+    }
+    std::vector<std::pair<std::string, std::uint64_t>> sorted(merged.begin(), merged.end());
+    std::sort(sorted.begin(), sorted.end(),
+              [](auto& x, auto& y) { return x.second != y.second ? x.second > y.second : x.first < y.first; });
+    std::string ser;
+    for (auto& [k, c] : sorted) ser += k + "\t" + std::to_string(c) + "\n";
+    std::vector<std::size_t> sizes;
+    for (const Element& e : d.collect()) sizes.push_back(e.size());
+    w["corpus"] = {{"seed", 5}, {"words", 30000}, {"bytes", corpus.size()}, {"target_chunk", 16384},
+                   {"chunk_sizes", sizes}, {"chunk_table_fnv", chunk_fnv}, {"merged_fnv", hex64(fnv64(ser.data(), ser.size()))},
+                   {"top3", json::array({{sorted[0].first, sorted[0].second}, {sorted[1].first, sorted[1].second},
+                                         {sorted[2].first, sorted[2].second}})},
+                   {"device_equals_host", same}};
+    g["wordcount"] = w;
+  }
+
   // Error behaviour
   {
     json e;

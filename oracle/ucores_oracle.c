@@ -216,6 +216,37 @@ void orc_sobel_band_u8(const uint8_t* in, uint64_t rows_out, uint64_t width, uin
   }
 }
 
+static inline int is_delim(uint8_t b) { return b == ' ' || b == '\t' || b == '\n' || b == '\r'; }
+
+/* WordCount run() body with the dataset.hpp:87-89 delimiters. */
+void orc_word_start_flags(const uint8_t* b, uint64_t n, uint8_t* flags) {
+  for (uint64_t i = 0; i < n; ++i) flags[i] = (uint8_t)(!is_delim(b[i]) && (i == 0 || is_delim(b[i - 1])));
+}
+
+/* ucores/dataset.hpp:94-112 chunk_offsets: a tentative cut at start+target is
+ * advanced past the next delimiter so no word spans two chunks. */
+uint64_t orc_chunk_offsets(const uint8_t* data, uint64_t n, uint64_t target, uint64_t* pairs, uint64_t max_chunks) {
+  uint64_t start = 0, k = 0;
+  while (start < n) {
+    const uint64_t tentative = start + target;
+    uint64_t cut;
+    if (tentative >= n) {
+      cut = n;
+    } else {
+      uint64_t d = tentative;
+      while (d < n && !is_delim(data[d])) ++d;
+      cut = d < n ? d + 1 : n;
+    }
+    if (k < max_chunks) {
+      pairs[2 * k] = start;
+      pairs[2 * k + 1] = cut;
+    }
+    ++k;
+    start = cut;
+  }
+  return k;
+}
+
 /* Matmul class-D body: C[gid] with gid = i*n + j, fp32 accumulate over k in
  * ascending order (workload C5; not in the reference). */
 void orc_matmul_f32(const float* A, const float* B, uint64_t n, float* C) {

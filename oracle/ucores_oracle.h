@@ -68,6 +68,14 @@ uint64_t orc_pi_hits(uint64_t task_seed, uint64_t samples);
  * zero. out(r,c) = min(255, |Gx|+|Gy|). */
 void orc_sobel_band_u8(const uint8_t* in, uint64_t rows_out, uint64_t width, uint8_t* out);
 
+/* ---- WordCount: flags[i] = byte i is a word character and
+ * (i == 0 or byte i-1 is a delimiter); delimiters: space, tab, LF, CR
+ * (ucores/dataset.hpp:87-89). */
+void orc_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* flags);
+/* create_from_text chunk boundaries (ucores/dataset.hpp:94-112): writes up to
+ * max_chunks [begin,end) pairs, returns the number of chunks. */
+uint64_t orc_chunk_offsets(const uint8_t* data, uint64_t n, uint64_t target, uint64_t* pairs, uint64_t max_chunks);
+
 /* ---- dense matmul: C = A·B (n×n row-major). fp32 sequential-k accumulate
  * (the class-D run() body) and an fp64 entry for tolerance checks. */
 void orc_matmul_f32(const float* A, const float* B, uint64_t n, float* C);

@@ -32,7 +32,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", str(INCLUDE),
                      "--expt-relaxed-constexpr"]
 
-CUDA_SOURCES = ["ucg_runtime.cu", "ucg_reduce.cu", "ucg_pi.cu", "ucg_sobel.cu", "ucg_gemm.cu"]
+CUDA_SOURCES = ["ucg_runtime.cu", "ucg_reduce.cu", "ucg_pi.cu", "ucg_sobel.cu", "ucg_gemm.cu", "ucg_text.cu"]
 
 
 def _nvcc() -> str:

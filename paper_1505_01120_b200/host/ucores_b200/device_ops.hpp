@@ -358,6 +358,52 @@ inline DeviceOp sobel(std::size_t width) {
   return op;
 }
 
+/// wordcount: word-start flags of every chunk on the GPU, tokens counted on
+/// the host from the flags (the kernel's map_return_value). Chunks below
+/// min_device_bytes take the kernel's own declared host path (selective
+/// execution) — the same table either way.
+inline DeviceOp wordcount(std::uint64_t min_device_bytes) {
+  DeviceOp op;
+  op.arity = ucores::KernelArity::Unary;
+  op.run_tasks = [min_device_bytes](Gpu& g, TaskBatch tasks) {
+    std::vector<std::span<const std::uint8_t>> in;
+    std::vector<std::uint64_t> sizes;
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+      in.push_back(detail::input_view<std::uint8_t>(tasks[i]->inputs.at(0), i));
+      sizes.push_back(in.back().size());
+    }
+    std::uint64_t total = 0;
+    const auto off = detail::pack_offsets(sizes, 16, &total);
+    std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(total));
+    std::uint8_t* dfl = static_cast<std::uint8_t*>(g.scratch(1).ensure(total));
+    for (std::size_t i = 0; i < in.size(); ++i) {
+      if (sizes[i] < min_device_bytes || !sizes[i]) continue;
+      g.h2d(din + off[i], in[i].data(), sizes[i]);
+      check(ucg_word_start_flags(din + off[i], sizes[i], dfl + off[i], g.stream()));
+    }
+    std::vector<std::uint8_t> flags(total);
+    g.d2h(flags.data(), dfl, total);
+    g.sync();
+    std::vector<ucores::Element> out;
+    for (std::size_t i = 0; i < in.size(); ++i) {
+      if (sizes[i] < min_device_bytes) out.push_back(kernels::WordCount::table_host(in[i]));
+      else out.push_back(kernels::WordCount::table_from_flags(in[i], flags.data() + off[i]));
+    }
+    return out;
+  };
+  op.run_phase = [](Gpu& g, ucores::KernelContext& ctx) {
+    auto in = ctx.buffer<std::uint8_t>("in");
+    auto fl = ctx.buffer<std::uint8_t>("flags");
+    std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(in.size() + 16));
+    std::uint8_t* dfl = static_cast<std::uint8_t*>(g.scratch(1).ensure(in.size() + 16));
+    g.h2d(din, in.data(), in.size());
+    check(ucg_word_start_flags(din, in.size(), dfl, g.stream()));
+    g.d2h(fl.data(), dfl, fl.size());
+    g.sync();
+  };
+  return op;
+}
+
 /// matmul: C = A.B per task on TF32 tensor cores (tolerance, not bit-exact).
 inline DeviceOp matmul_tf32(std::size_t n) {
   DeviceOp op;
@@ -396,11 +442,12 @@ struct WorkloadParams {
   float a = 2.0f, b = 1.0f;     // axpb
   std::size_t sobel_width = 16384;
   std::size_t matmul_n = 8192;
+  std::uint64_t wordcount_min_device_bytes = 65536;  // EngineConfig::min_device_bytes (engine.hpp:18)
 };
 
 /// Registers the host kernels (reference API) and their device bodies under
 /// the same names: axpb, psum, pmax, sum2, vectoradd, max2, isum2, pi,
-/// sobel, matmul.
+/// sobel, matmul, wordcount.
 inline void register_workload(ucores::KernelRegistry& reg, DeviceOpRegistry& ops, const WorkloadParams& p = {}) {
   using namespace kernels;
   reg.register_unary("axpb", [p] { return std::make_unique<Axpb>(p.a, p.b); });
@@ -413,6 +460,8 @@ inline void register_workload(ucores::KernelRegistry& reg, DeviceOpRegistry& ops
   reg.register_unary("pi", [] { return std::make_unique<Pi>(); });
   reg.register_unary("sobel", [p] { return std::make_unique<Sobel>(p.sobel_width); });
   reg.register_unary("matmul", [p] { return std::make_unique<Matmul>(p.matmul_n); });
+  reg.register_unary("wordcount", [p] { return std::make_unique<WordCount>(p.wordcount_min_device_bytes); });
+  ops.add("wordcount", device_ops::wordcount(p.wordcount_min_device_bytes));
   ops.add("axpb", device_ops::affine_f32(p.a, p.b));
   ops.add("psum", device_ops::partition_reduce_f32(ReduceOp::Sum));
   ops.add("pmax", device_ops::partition_reduce_f32(ReduceOp::Max));

@@ -13,12 +13,14 @@
 //   pi        params {seed, samples} (i64) -> hits (u8, samples) range samples
 //   sobel     in (u8, (rows+2)*w)     -> out (u8, rows*w)    range rows*w
 //   matmul    ab (f32, 2n^2)          -> c (f32, n^2)        range n^2
+//   wordcount in (u8, chunk)          -> flags (u8, chunk)   range chunk bytes
 #pragma once
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
 #include <memory>
 #include <span>
 #include <string>
@@ -228,6 +230,90 @@ class Sobel : public ucores::UnaryKernel {
  private:
   std::size_t w_, rows_ = 0;
   std::span<std::uint8_t> in_, out_;
+};
+
+/// WordCount: ByteArray chunk -> KeyCountTable. run() marks
+/// word starts (class D, the "local data" flags buffer); map_return_value
+/// walks the flags to cut tokens and counts them, keys in order of first
+/// occurrence. Chunks below min_device_bytes decline device execution and
+/// tokenize on the host (selective execution).
+class WordCount : public ucores::UnaryKernel {
+ public:
+  static bool is_delim(std::uint8_t b) { return b == ' ' || b == '\t' || b == '\n' || b == '\r'; }
+  explicit WordCount(std::uint64_t min_device_bytes) : min_(min_device_bytes) {}
+  void map_parameters(ucores::KernelContext& ctx, const ucores::Element& in) override {
+    bytes_ = in.as_bytes();
+    ctx.set_range(bytes_.size());
+    if (bytes_.size() < min_) {
+      ctx.set_device_execution(false);
+      return;
+    }
+    ctx.bind<std::uint8_t>("in", bytes_);
+    flags_ = ctx.alloc<std::uint8_t>("flags", bytes_.size());
+  }
+  void run(ucores::KernelContext&, std::size_t gid) override {
+    flags_[gid] = static_cast<std::uint8_t>(!is_delim(bytes_[gid]) && (gid == 0 || is_delim(bytes_[gid - 1])));
+  }
+  ucores::Element map_return_value(ucores::KernelContext& ctx, const ucores::Element&) override {
+    if (ctx.device_execution()) {
+      std::vector<std::uint8_t> f = ctx.take<std::uint8_t>("flags");
+      return table_from_flags(bytes_, f.data());
+    }
+    return table_host(bytes_);  // "alternative compute function" on the host
+  }
+
+  /// Tokens cut at the flagged word starts, counted, keys in first-occurrence order.
+  static ucores::Element table_from_flags(std::span<const std::uint8_t> bytes, const std::uint8_t* flags) {
+    Counter c(bytes);
+    const std::size_t n = bytes.size();
+    for (std::size_t i = 0; i < n; ++i) {
+      if (!flags[i]) continue;
+      std::size_t e = i;
+      while (e < n && !is_delim(bytes[e])) ++e;
+      c.add(i, e);
+      i = e;
+    }
+    return c.done();
+  }
+  /// The same table by direct host tokenisation.
+  static ucores::Element table_host(std::span<const std::uint8_t> bytes) {
+    Counter c(bytes);
+    const std::size_t n = bytes.size();
+    for (std::size_t i = 0; i < n;) {
+      while (i < n && is_delim(bytes[i])) ++i;
+      std::size_t e = i;
+      while (e < n && !is_delim(bytes[e])) ++e;
+      if (e > i) c.add(i, e);
+      i = e;
+    }
+    return c.done();
+  }
+
+ private:
+  struct Counter {
+    std::span<const std::uint8_t> bytes;
+    std::vector<std::pair<std::string, std::uint64_t>> table;
+    std::map<std::string, std::size_t, std::less<>> index;
+    explicit Counter(std::span<const std::uint8_t> b) : bytes(b) {}
+    void add(std::size_t b, std::size_t e) {
+      std::string key(reinterpret_cast<const char*>(bytes.data()) + b, e - b);
+      auto it = index.find(key);
+      if (it == index.end()) {
+        index.emplace(key, table.size());
+        table.emplace_back(std::move(key), 1);
+      } else {
+        table[it->second].second += 1;
+      }
+    }
+    ucores::Element done() { return ucores::Element::table(std::move(table)); }
+  };
+
+ public:
+
+ private:
+  std::uint64_t min_;
+  std::span<const std::uint8_t> bytes_;
+  std::span<std::uint8_t> flags_;
 };
 
 /// Dense matmul (C5): F32Array A||B (2n^2) -> C = A.B (fp32, k ascending).

@@ -120,6 +120,13 @@ def sobel_bands(inp, in_off: Sequence[int], out, out_off: Sequence[int], rows: S
     return out
 
 
+def word_start_flags(data, flags, stream=None):
+    """wordcount run() over one chunk: 1 at every byte that starts a word."""
+    _require_cuda(data, flags)
+    call("ucg_word_start_flags", ptr(data), data.numel(), ptr(flags), stream_handle(stream))
+    return flags
+
+
 def gemm_tf32(A, B, Cm, n: int, stream=None):
     _require_cuda(A, B, Cm)
     call("ucg_gemm_tf32", ptr(A), ptr(B), ptr(Cm), n, stream_handle(stream))

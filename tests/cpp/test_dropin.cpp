@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <fstream>
 #include <functional>
 #include <string>
 #include <vector>
@@ -287,6 +288,39 @@ int main() {
         EXPECT(md <= 1e-2 * std::sqrt(ss / a.size()), "matmul within TF32 tolerance");
       }
     }
+  });
+
+  run_case("wordcount over create_from_text chunks: GPU flags (seam A, B) == host tables", [&] {
+    std::string corpus;
+    const char dl[4] = {' ', '\t', '\n', '\r'};
+    for (std::size_t i = 0; i < 30000; ++i) {
+      const std::uint64_t z = kernels::mix64(5 + i);
+      corpus += "w" + std::to_string(z % 97);
+      corpus.append(1 + ((z >> 40) & 1), dl[(z >> 32) & 3]);
+    }
+    const std::string path = "/tmp/ucores_b200_wc.txt";
+    {
+      std::ofstream f(path, std::ios::binary);
+      f << corpus;
+    }
+    Dataset d = create_from_text(path, 16384);
+    KernelRegistry reg0;
+    DeviceOpRegistry ops0;
+    WorkloadParams p0;
+    p0.wordcount_min_device_bytes = 0;  // every chunk takes the device path
+    register_workload(reg0, ops0, p0);
+    HostDriver h0(reg0);
+    GpuClusterDriver g0(reg0, ops0);
+    GpuClusterDriver::Options pt;
+    pt.mode = GpuClusterDriver::Mode::PerTask;
+    GpuClusterDriver b0(reg0, ops0, pt);
+    Engine eh0(h0, reg0), eg0(g0, reg0), eb0(b0, reg0);
+    Dataset host = eh0.map_cl(d, "wordcount");
+    EXPECT(same(host, eg0.map_cl(d, "wordcount")), "seam A tables equal");
+    EXPECT(same(host, eb0.map_cl(d, "wordcount")), "seam B tables equal");
+    // default threshold 65536 > 16 KB chunks: all chunks decline the device
+    Dataset fb = eg.map_cl(d, "wordcount");
+    EXPECT(same(host, fb), "selective-execution path equal");
   });
 
   run_case("no device body -> JobFailed (no CPU fallback)", [&] {

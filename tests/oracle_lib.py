@@ -38,6 +38,8 @@ def lib() -> C.CDLL:
             "orc_sobel_band_u8": (None, [vp, u64, u64, vp]),
             "orc_matmul_f32": (None, [vp, vp, u64, vp]),
             "orc_matmul_entry_f64": (C.c_double, [vp, vp, u64, u64, u64]),
+            "orc_word_start_flags": (None, [vp, u64, vp]),
+            "orc_chunk_offsets": (u64, [vp, u64, u64, vp, u64]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -167,6 +169,60 @@ def sobel_bands(img: np.ndarray, rows: int) -> list[np.ndarray]:
                 b[k] = img[src]
         bands.append(b)
     return bands
+
+
+def word_start_flags(data: bytes) -> np.ndarray:
+    b = np.frombuffer(data, dtype=np.uint8).copy()
+    out = np.empty(b.size, dtype=np.uint8)
+    lib().orc_word_start_flags(_p(b), b.size, _p(out))
+    return out
+
+
+def chunk_offsets(data: bytes, target: int) -> list[tuple[int, int]]:
+    b = np.frombuffer(data, dtype=np.uint8).copy()
+    cap = len(data) // max(1, target) + 2
+    pairs = np.zeros(2 * cap, dtype=np.uint64)
+    k = int(lib().orc_chunk_offsets(_p(b), b.size, target, _p(pairs), cap))
+    return [(int(pairs[2 * i]), int(pairs[2 * i + 1])) for i in range(k)]
+
+
+def corpus(seed: int, words: int) -> bytes:
+    """Synthetic text shared with oracle/ref_harness.cpp make_corpus."""
+    dl = b" \t\n\r"
+    out = bytearray()
+    for i in range(words):
+        z = mix64(seed + i)
+        out += b"w" + str(z % 97).encode()
+        out += bytes([dl[(z >> 32) & 3]]) * (1 + ((z >> 40) & 1))
+    return bytes(out)
+
+
+def word_table(chunk: bytes, flags=None) -> list[tuple[bytes, int]]:
+    """KeyCountTable of one chunk, keys in first-occurrence order (from flags
+    when given, else by direct tokenisation) — small inputs only."""
+    delim = set(b" \t\n\r")
+    order, counts = [], {}
+    n = len(chunk)
+    starts = [i for i in range(n) if flags[i]] if flags is not None else None
+    if starts is None:
+        starts, i = [], 0
+        while i < n:
+            while i < n and chunk[i] in delim:
+                i += 1
+            if i < n:
+                starts.append(i)
+            while i < n and chunk[i] not in delim:
+                i += 1
+    for s in starts:
+        e = s
+        while e < n and chunk[e] not in delim:
+            e += 1
+        k = chunk[s:e]
+        if k not in counts:
+            order.append(k)
+            counts[k] = 0
+        counts[k] += 1
+    return [(k, counts[k]) for k in order]
 
 
 def f32_bits(v) -> str:
