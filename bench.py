@@ -299,6 +299,8 @@ def our_arm(args, world, rank, local):
     achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
     peak, peak_kind = load_peak()
     traffic = load_traffic("fused_pass1_bytes_per_launch" if not args.no_fuse else "unfused_bytes_per_step")
+    if traffic is not None:  # the ncu capture is at 2^30 elements on one GPU: scale to this launch
+        traffic = int(traffic * local_elems / float(1 << 30))
 
     # ---- e2e through the unmodified reference ucores::Engine + GpuClusterDriver -------
     engine_e2e = None

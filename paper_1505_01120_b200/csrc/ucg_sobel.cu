@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ucg_common.cuh"
@@ -163,6 +164,177 @@ __global__ void __launch_bounds__(kSobelThreads)
   }
 }
 
+// ---- TMA-tiled path -----------------------------------------------------------
+// A CTA tile is 256 output columns x 64 output rows of one band. TMA copies the
+// 66 x 256 input rows plus 16-byte side boxes at x-16 and x+256 into shared
+// memory; side boxes that fall outside the image are zero-filled by the TMA
+// unit, which is exactly the zero-outside-columns rule. Persistent CTAs double
+// buffer: the tile after next is requested as soon as a buffer is free. Each
+// of the 128 threads owns 16 columns x 8 output rows (10 input rows, 3-row
+// window in registers), reads its bytes with LDS.128 and the neighbour bytes
+// from the side columns, and stores 16 output bytes per row.
+constexpr int kTW = 256, kTH = 64, kTIn = kTH + 2;
+constexpr uint32_t kCenterBytes = kTW * kTIn;          // 16896
+constexpr uint32_t kSideBytes = 16 * kTIn;             // 1056
+constexpr uint32_t kSideStride = 1152;                 // side boxes at 128-byte aligned offsets
+constexpr uint32_t kBufBytes = 19200;                  // center + 2 sides, 128-aligned
+constexpr int kTmaThreads = 128;
+
+struct SobelTiles {
+  uint32_t in_row0[kMaxBands];      // first input row of band b in the 2-D view
+  uint64_t out_off[kMaxBands];
+  uint32_t rows[kMaxBands];
+  uint32_t first_tile[kMaxBands + 1];
+  uint32_t nbands;
+  uint32_t col_tiles;
+};
+
+__device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+// d = a*b + c on the FMA pipe (IMAD), leaving the ALU pipe to PRMT / VIMNMX
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ void tile_of(const SobelTiles& p, uint32_t t, uint32_t& b, uint32_t& rb, uint32_t& cb) {
+  uint32_t lo = 0, hi = p.nbands;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (p.first_tile[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  b = lo;
+  const uint32_t k = t - p.first_tile[lo];
+  rb = k / p.col_tiles;
+  cb = k % p.col_tiles;
+}
+
+struct SobelMaps {
+  CUtensorMap center;  // box {256 B, 66 rows}
+  CUtensorMap side;    // box {16 B, 66 rows}
+};
+
+__device__ __forceinline__ void issue_tile(const SobelMaps* maps, const SobelTiles& p, uint32_t t, uint8_t* buf,
+                                           uint64_t* bar) {
+  uint32_t b, rb, cb;
+  tile_of(p, t, b, rb, cb);
+  const int x = int(cb) * kTW, y = int(p.in_row0[b] + rb * kTH);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)),
+               "r"(kCenterBytes + 2 * kSideBytes) : "memory");
+  const int xs[3] = {x, x - 16, x + kTW};
+  const uint32_t dst[3] = {sa(buf), sa(buf + kCenterBytes), sa(buf + kCenterBytes + kSideStride)};
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst[k]), "l"(k ? &maps->side : &maps->center), "r"(xs[k]), "r"(y), "r"(sa(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads)
+    k_sobel_tma(const __grid_constant__ SobelMaps maps, uint8_t* __restrict__ out, const __grid_constant__ SobelTiles p,
+                uint64_t width, uint32_t ntiles) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x, cg = tid & 15, rg = tid >> 4;
+  const SobelMaps* map = &maps;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&full[0])), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&full[1])), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  if (tid == 0) {
+    if (blockIdx.x < ntiles) issue_tile(map, p, blockIdx.x, smem, &full[0]);
+    if (blockIdx.x + gridDim.x < ntiles) issue_tile(map, p, blockIdx.x + gridDim.x, smem + kBufBytes, &full[1]);
+  }
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const uint32_t bi = it & 1;
+    uint8_t* buf = smem + bi * kBufBytes;
+    asm volatile("{\n .reg .pred q;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n @!q bra W;\n}\n" ::"r"(
+                     sa(&full[bi])), "r"((it >> 1) & 1)
+                 : "memory");
+    uint32_t b, rb, cb;
+    tile_of(p, t, b, rb, cb);
+    const uint32_t valid_rows = min(uint32_t(kTH), p.rows[b] - rb * kTH);
+    const uint64_t col = uint64_t(cb) * kTW + cg * 16;
+    const uint8_t* center = buf;
+    const uint8_t* left = buf + kCenterBytes;
+    const uint8_t* right = left + kSideStride;
+    // smem reads through explicit shared-window addresses (LDS, not generic LD)
+    const uint32_t c_s = sa(center), l_s = sa(left), r_s = sa(right);
+    auto terms = [&](int i, RowTerms& tr) {
+      const uint32_t row = c_s + uint32_t(i * kTW + cg * 16);
+      uint4 w;
+      uint32_t lft, rgt;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(row));
+      const uint32_t la = cg ? row - 1 : l_s + uint32_t(i * 16 + 15);
+      const uint32_t ra = cg < 15 ? row + 16 : r_s + uint32_t(i * 16);
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(lft) : "r"(la));
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(rgt) : "r"(ra));
+      const uint32_t ws[6] = {lft << 24, w.x, w.y, w.z, w.w, rgt};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t cur = ws[k + 1];
+        const uint32_t sl = __byte_perm(ws[k], cur, 0x6543);
+        const uint32_t sr = __byte_perm(cur, ws[k + 2], 0x4321);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t sel = h ? 0x4342u : 0x4140u;
+          // E, L: bytes -> 16-bit halves; Rb = R + 256 per half (the 0x01 filler bytes)
+          const uint32_t E = __byte_perm(cur, 0, sel), L = __byte_perm(sl, 0, sel);
+          const uint32_t Rb = __byte_perm(sr, 0x01010101u, sel);
+          // half the adds on the FMA pipe (IMAD), the byte permutes/min/max on the ALU pipe
+          tr.dh[2 * k + h] = mad_u32(L, 0xFFFFFFFFu, Rb);       // R - L + 256
+          tr.sh[2 * k + h] = mad_u32(E, 2u, L + Rb);            // L + 2E + R + 256
+        }
+      }
+    };
+    uint8_t* dst = out + p.out_off[b] + (uint64_t(rb) * kTH + rg * 8) * width + col;
+    auto emit = [&](int r, const RowTerms& a, const RowTerms& bb, const RowTerms& c) {
+      if (uint32_t(rg * 8 + r) >= valid_rows || col >= width) return;
+      uint32_t o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t gx = mad_u32(bb.dh[i], 2u, a.dh[i] + c.dh[i]);   // Gx + 1024
+        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;             // Gy + 1024
+        const uint32_t ax = __vmaxu2(gx, mad_u32(gx, 0xFFFFFFFFu, 0x08000800u));
+        const uint32_t ay = __vmaxu2(gy, mad_u32(gy, 0xFFFFFFFFu, 0x08000800u));
+        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);
+      }
+      const uint32_t q0 = __byte_perm(o[0], o[1], 0x6420), q1 = __byte_perm(o[2], o[3], 0x6420);
+      const uint32_t q2 = __byte_perm(o[4], o[5], 0x6420), q3 = __byte_perm(o[6], o[7], 0x6420);
+      st_stream(reinterpret_cast<float4*>(dst + uint64_t(r) * width),
+                make_float4(__uint_as_float(q0), __uint_as_float(q1), __uint_as_float(q2), __uint_as_float(q3)));
+    };
+    const int i0 = rg * 8;
+    RowTerms t0, t1, t2;
+    terms(i0, t0);
+    terms(i0 + 1, t1);
+    terms(i0 + 2, t2);
+    emit(0, t0, t1, t2);
+    terms(i0 + 3, t0);
+    emit(1, t1, t2, t0);
+    terms(i0 + 4, t1);
+    emit(2, t2, t0, t1);
+    terms(i0 + 5, t2);
+    emit(3, t0, t1, t2);
+    terms(i0 + 6, t0);
+    emit(4, t1, t2, t0);
+    terms(i0 + 7, t1);
+    emit(5, t2, t0, t1);
+    terms(i0 + 8, t2);
+    emit(6, t0, t1, t2);
+    terms(i0 + 9, t0);
+    emit(7, t1, t2, t0);
+    __syncthreads();  // buffer bi fully read
+    if (tid == 0 && t + 2 * gridDim.x < ntiles) issue_tile(map, p, t + 2 * gridDim.x, buf, &full[bi]);
+  }
+}
+
 // Generic path for widths that are not a multiple of 16 (rows not 16-byte
 // aligned): one thread per output pixel, nine byte loads.
 __global__ void __launch_bounds__(256)
@@ -207,6 +379,53 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
   cudaStream_t st = as_stream(stream);
   bool vec = width % 16 == 0 && aligned16(in) && aligned16(out);
   for (uint64_t i = 0; i < nbands && vec; ++i) vec = in_off[i] % 16 == 0 && out_off[i] % 16 == 0;
+  bool tma = vec && width >= 16 && width < (1ull << 31) && !getenv("UCG_SOBEL_NO_TMA");
+  uint64_t total_rows = 0;
+  for (uint64_t i = 0; i < nbands && tma; ++i) {
+    tma = in_off[i] % width == 0 && rows[i] < (1u << 30);
+    total_rows = std::max<uint64_t>(total_rows, in_off[i] / width + rows[i] + 2);
+  }
+  if (tma && total_rows < (1ull << 31)) {
+    auto enc = tmap_encode_fn();
+    if (!enc) return fail(UCG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    SobelMaps maps;
+    cuuint64_t dims[2] = {width, total_rows};
+    cuuint64_t strides[1] = {width};
+    cuuint32_t estr[2] = {1, 1};
+    cuuint32_t boxc[2] = {uint32_t(kTW), uint32_t(kTIn)}, boxs[2] = {16u, uint32_t(kTIn)};
+    CUresult r1 = enc(&maps.center, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(in), dims, strides, boxc,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r2 = enc(&maps.side, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(in), dims, strides, boxs,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) return fail(UCG_ERR_CUDA, "sobel tensor map encode failed");
+    static bool attr = false;
+    if (!attr) {
+      UCG_CUDA(cudaFuncSetAttribute(k_sobel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * kBufBytes + 128)));
+      attr = true;
+    }
+    const uint32_t col_tiles = uint32_t((width + kTW - 1) / kTW);
+    for (uint64_t b0 = 0; b0 < nbands; b0 += kMaxBands) {
+      const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));
+      SobelTiles p;
+      p.nbands = nb;
+      p.col_tiles = col_tiles;
+      p.first_tile[0] = 0;
+      for (uint32_t i = 0; i < nb; ++i) {
+        p.in_row0[i] = uint32_t(in_off[b0 + i] / width);
+        p.out_off[i] = out_off[b0 + i];
+        p.rows[i] = uint32_t(rows[b0 + i]);
+        p.first_tile[i + 1] = p.first_tile[i] + uint32_t((rows[b0 + i] + kTH - 1) / kTH) * col_tiles;
+      }
+      const uint32_t ntiles = p.first_tile[nb];
+      if (!ntiles) continue;
+      const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count()) * 5));
+      k_sobel_tma<<<grid, kTmaThreads, 2 * kBufBytes + 128, st>>>(maps, out, p, width, ntiles);
+      UCG_LAUNCHED();
+    }
+    return UCG_OK;
+  }
   for (uint64_t b0 = 0; b0 < nbands; b0 += kMaxBands) {
     const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));
     SobelBands p;
