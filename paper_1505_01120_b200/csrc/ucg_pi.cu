@@ -3,11 +3,10 @@
 // Per sample gid of task t: s0 = seed ^ gid*GAMMA, z1 = mix64(s0+GAMMA),
 // z2 = mix64(s0+2*GAMMA), a = z1>>32, b = z2>>32, and the reference test is
 //   fl(fl(x*x) + fl(y*y)) <= 1.0   with x = a/2^32, y = b/2^32 in IEEE double.
-// Here x*x = fl(a^2)*2^-64 exactly, so the test is decided in integers from
-// the exact S = a^2 + b^2 (65 bits): the double evaluation differs from S by
-// less than 2^13, hence S <= 2^64 - 2^14 is a certain hit and S >= 2^64 + 2^14
-// a certain miss; the band in between (probability ~1e-15) re-evaluates the
-// exact double expression with __dmul_rn / __dadd_rn (no FMA contraction).
+// Here x*x = fl(a^2)*2^-64 exactly, so the test is evaluated on the FP64
+// pipe as fl(fl(a^2)+fl(b^2)) <= 2^64 (__dmul_rn / __dadd_rn: no FMA
+// contraction), leaving the integer ALU pipe to the SplitMix64 shifts/xors;
+// 64-bit adds run as IMAD.WIDE on the FMA pipe.
 // Counts: ballot-free integer accumulation, warp redux, one 64-bit atomic per
 // CTA per 64Ki-sample work unit.
 #include <cuda_runtime.h>
@@ -31,18 +30,33 @@ struct PiTasks {
   uint32_t ntasks;
 };
 
+// 64-bit x + c with the add on the FMA pipe (IMAD.WIDE.U32 + IMAD): the
+// SplitMix64 shifts / xors already saturate the integer ALU pipe.
+__device__ __forceinline__ uint64_t add64_fma(uint64_t x, uint64_t c) {
+  uint64_t lo;
+  asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(lo) : "r"(uint32_t(x)), "l"(c));
+  uint32_t hi;
+  asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(hi) : "r"(uint32_t(x >> 32)), "r"(uint32_t(lo >> 32)));
+  return (uint64_t(hi) << 32) | uint32_t(lo);
+}
+
+// High 32 bits of mix64(z): the last step z ^ (z >> 31) only feeds bit 63
+// of z into the high word, so hi32 = hi(z) ^ (hi(z) >> 31).
+__device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const uint32_t h = uint32_t(z >> 32);
+  return h ^ (h >> 31);
+}
+
+// Exact reference test on the FP64 pipe (separate from the integer ALU):
+// x*x = fl(a^2)*2^-64 exactly, so fl(fl(x*x)+fl(y*y)) <= 1 is
+// fl(fl(a^2)+fl(b^2)) <= 2^64 with a, b converted exactly to double.
 __device__ __forceinline__ uint32_t pi_hit(uint64_t s0) {
-  const uint64_t z1 = mix64(s0 + kGamma);
-  const uint64_t z2 = mix64(s0 + 2 * kGamma);
-  const uint32_t a = uint32_t(z1 >> 32), b = uint32_t(z2 >> 32);
-  const uint64_t A = uint64_t(a) * a, B = uint64_t(b) * b;
-  const uint64_t lo = A + B;
-  const bool carry = lo < A;
-  if (!carry && lo < 0xFFFFFFFFFFFFC000ull) return 1u;  // S <= 2^64 - 2^14
-  if (carry && lo >= (1ull << 14)) return 0u;           // S >= 2^64 + 2^14
-  const double x = double(a) * (1.0 / 4294967296.0);
-  const double y = double(b) * (1.0 / 4294967296.0);
-  return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)) <= 1.0 ? 1u : 0u;
+  const uint32_t a = mix64_hi(add64_fma(s0, kGamma));
+  const uint32_t b = mix64_hi(add64_fma(s0, 2 * kGamma));
+  const double da = __uint2double_rn(a), db = __uint2double_rn(b);
+  return __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)) <= 18446744073709551616.0 ? 1u : 0u;
 }
 
 __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTasks tasks, uint64_t nunits,
@@ -67,7 +81,7 @@ __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTas
 #pragma unroll 4
       for (int i = 0; i < (1 << kUnitLog2) / kPiThreads; ++i) {
         cnt += pi_hit(seed ^ m);
-        m += mstep;
+        m = add64_fma(m, mstep);
       }
     } else {
       for (; gid < end; gid += kPiThreads) {
