@@ -311,6 +311,185 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ---- CTA-pair (cta_group::2) variant -----------------------------------------
+// A cluster of 2 CTAs on one TPC computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M=256): each CTA stages ITS 128 rows of A and
+// ITS 128 columns of B (32 KB per stage instead of 48 KB) and owns 128 rows
+// of the accumulator in its TMEM; the leader CTA issues the MMAs. Both CTAs'
+// TMA loads complete on the leader's full barrier (.cta_group::2 form, peer
+// bit cleared); MMA commits multicast to both CTAs' empty / tmem-full
+// barriers; both CTAs' epilogues arrive on the leader's tmem-empty barrier.
+constexpr int S2 = 6;                                // stages
+constexpr uint32_t A2_BYTES = 128 * BK * 4;          // 16 KB: this CTA's 128 rows
+constexpr uint32_t B2_BYTES = 4 * B_STRIP;           // 16 KB: this CTA's 128 columns
+constexpr uint32_t STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr uint32_t SMEM2_BYTES = S2 * STAGE2_BYTES + 1024;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;          // shared::cluster address of the even (leader) CTA
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) | (uint32_t(256 >> 3) << 17) |
+                             (uint32_t(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_2d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc2), "r"(accumulate), "r"(0u));
+}
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_addr(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    k_gemm_tf32_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    float* __restrict__ C, int n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[S2], empty[S2], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tiles_m = n / 256, tiles_n = n / 256, ntiles = tiles_m * tiles_n, nk = n / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);  // both CTAs' 128 epilogue threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int t = pair; t < ntiles; t += npairs) {
+        int mb, nb;
+        {  // grouped raster over 256 x 256 tiles
+          const int per_group = kGroupM * tiles_n;
+          const int g = t / per_group, idx = t % per_group;
+          const int gm = min(kGroupM, tiles_m - g * kGroupM);
+          mb = g * kGroupM + idx % gm;
+          nb = idx / gm;
+        }
+        const int m0 = mb * 256 + int(rank) * 128, n0 = nb * 256 + int(rank) * 128;
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = int(q % S2);
+          if (q >= uint32_t(S2)) mbar_wait(&empty[s], ((q / S2) & 1) ^ 1);
+          uint8_t* a = smem + s * STAGE2_BYTES;
+          uint8_t* b = a + A2_BYTES;
+          const uint32_t lbar = smem_addr(&full[s]) & kPeerMask;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
+          tma_2d_2sm(a, &tmA, lbar, kb * BK, m0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma_2d_2sm(b + j * B_STRIP, &tmB, lbar, n0 + 32 * j, kb * BK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      uint32_t q = 0, i = 0;
+      for (int t = pair; t < ntiles; t += npairs, ++i) {
+        const uint32_t acc = i & 1;
+        if (i >= 2) mbar_wait(&tempty[acc], ((i / 2) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * 256u;
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = int(q % S2);
+          mbar_wait(&full[s], (q / S2) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a = smem_addr(smem + s * STAGE2_BYTES);
+          const uint32_t b = a + A2_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t adesc = smem_desc(a + 32u * k, 16u, 1024u, 2u);
+            const uint64_t bdesc = smem_desc(b + 1024u * k, B_STRIP, 512u, 1u);
+            mma_tf32_2sm(d, adesc, bdesc, (kb | k) != 0);
+          }
+          mma_commit_2sm(&empty[s]);
+        }
+        mma_commit_2sm(&tfull[acc]);
+      }
+    }
+  } else {
+    const int lg = warp & 3;
+    const uint32_t leader_tempty[2] = {smem_addr(&tempty[0]) & kPeerMask, smem_addr(&tempty[1]) & kPeerMask};
+    uint32_t i = 0;
+    for (int t = pair; t < ntiles; t += npairs, ++i) {
+      int mb, nb;
+      {
+        const int per_group = kGroupM * tiles_n;
+        const int g = t / per_group, idx = t % per_group;
+        const int gm = min(kGroupM, tiles_m - g * kGroupM);
+        mb = g * kGroupM + idx % gm;
+        nb = idx / gm;
+      }
+      const uint32_t acc = i & 1;
+      mbar_wait(&tfull[acc], (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float* crow = C + size_t(mb * 256 + int(rank) * 128 + lg * 32 + lane) * n + nb * 256;
+#pragma unroll 1
+      for (int c = 0; c < 256 / 32; ++c) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + (uint32_t(lg * 32) << 16) + acc * 256u + uint32_t(c * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+              "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float4* dst = reinterpret_cast<float4*>(crow + c * 32);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          __stcs(dst + qq, make_float4(__uint_as_float(r[4 * qq]), __uint_as_float(r[4 * qq + 1]),
+                                       __uint_as_float(r[4 * qq + 2]), __uint_as_float(r[4 * qq + 3])));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_tempty[acc]) : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() { return tmap_encode_fn(); }
 
 int make_map(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
@@ -344,7 +523,7 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   if (int rc = make_map(&tmB, B, n, n, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return rc;   // B[k][n]: inner n, box {32 n, 32 k}
   static const int variant = [] {
     const char* e = getenv("UCG_GEMM_VARIANT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;  // default: CTA-pair (cta_group::2) kernel
   }();
   static bool attr = false;
   if (!attr) {
@@ -355,6 +534,15 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   if (variant == 0) {
     dim3 grid(unsigned(n / BN), unsigned(n / BM));
     k_gemm_tf32<<<grid, 128, SMEM_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
+  } else if (variant == 2) {
+    static bool attr2 = false;
+    if (!attr2) {
+      UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+      attr2 = true;
+    }
+    const uint64_t ntiles = (n / 256) * (n / 256);
+    const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count() / 2))) * 2;
+    k_gemm_tf32_2sm<<<grid, 192, SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
   } else {
     const uint64_t ntiles = (n / BM) * (n / BN);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count())));
