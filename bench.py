@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-engine-e2e", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="c2 (default) is the headline; the others are the remaining BASELINE configs")
     ap.add_argument("--cpu-sample-parts", type=int, default=4)
     return ap.parse_args()
 
@@ -368,6 +370,10 @@ def main():
     world, rank, local = dist_env()
     if args.impl == "reference":
         return reference_arm(args, world, rank)
+    if args.workload != "c2":
+        import bench_configs
+
+        return bench_configs.run(args, world, rank, local)
     return our_arm(args, world, rank, local)
 
 

@@ -1,0 +1,241 @@
+"""The other BASELINE.json configs, measured with the same contract as
+bench.py (imported by `bench.py --workload c1|c3|c4|c5`):
+
+  c1  mapCL axpb over a 2^20-element collection in 4 partitions, then
+      mapCLPartition psum + reduceCL sum2 (the CPU-runnable case)
+  c3  Monte-Carlo pi via mapCL, 2^34 samples in 64 tasks (exact counts)
+  c4  mapCLPartition 3x3 Sobel on a 16384x16384 u8 image in 64 row bands
+  c5  mapCL dense fp32 matmul 8192^3 per partition, 8 partitions, tcgen05
+
+Units (tasks / bands / partitions) are split over the ranks in contiguous
+blocks; value = all units / max-over-ranks device time. The reference CPU
+path (oracle/_ref/ref_harness bench-workload) is timed on a bounded sample.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import subprocess
+import time
+
+import torch
+
+import bench as B
+from paper_1505_01120_b200 import capi, ops
+from paper_1505_01120_b200.pipeline import MapReducePipeline, shard_range
+
+CONFIGS = json.loads((B.ROOT / "BASELINE.json").read_text())["configs"]
+
+
+def _timed(fn, k, barrier):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(k):
+        fn()
+    e1.record()
+    barrier()
+    return e0.elapsed_time(e1) / k
+
+
+def _max_over_ranks(vals, world, dev):
+    if world == 1:
+        return vals
+    import torch.distributed as dist
+
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
+
+def _ref_workload(argv, timeout=900):
+    out = subprocess.run([str(B.REF_HARNESS), "bench-workload"] + argv + ["--threads", str(os.cpu_count() or 1)],
+                         check=True, capture_output=True, text=True, timeout=timeout).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def _line(args, world, workload, metric_desc, value, unit, step_ms, launches, clk, e2e, roofline, cpu, config):
+    return {"metric": f"{B.METRIC} [{workload}: {metric_desc}]", "value": value, "unit": unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": config.pop("dtype"), "data": "synthetic",
+            "config": config, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clk.summary()}
+
+
+def run(args, world, rank, local):
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    capi.load()
+    peak_hbm, peak_kind = B.load_peak()
+    k, w = args.steps, max(3, args.warmup)
+    cpu = None
+    line = None
+    if args.workload == "c1":
+        lens = [1 << 18] * 4
+        pipe = MapReducePipeline(lens, world=world, rank=rank, device=dev, plant_max=False)
+        for _ in range(w):
+            pipe.step()
+        with B.ClockSampler(local) as clk:
+            l0 = capi.launch_count()
+            ms = _timed(pipe.step, k, barrier)
+            launches = capi.launch_count() - l0
+            kern = _timed(pipe.map_and_partials, k, barrier)
+        pipe.setup_host_input(chunks=4)
+        for _ in range(2):
+            pipe.step_from_host()
+        e2e_ms = _timed(pipe.step_from_host, k, barrier)
+        ms, kern, e2e_ms = _max_over_ranks([ms, kern, e2e_ms], world, dev)
+        n = pipe.elements
+        if rank == 0 and world == 1:
+            r = B.run_ref_harness(4, 1 << 18, 3, 1, "sum", os.cpu_count() or 1)
+            cpu = {"value": r["elements"] / statistics.median(r["step_s"]), "unit": "elements/s",
+                   "cores": os.cpu_count(), "kind": "reference", "sample": "the full C1 workload (2^20 fp32, 4 partitions)"}
+        achieved = 8 * pipe.local_elements / (kern * 1e-3) / 1e9
+        line = _line(args, world, "c1", CONFIGS[0], n / (ms * 1e-3), "elements/s", ms, launches, clk,
+                     {"value": n / (e2e_ms * 1e-3), "unit": "elements/s", "h2d_bytes_per_step": pipe.h2d_bytes * world,
+                      "d2h_bytes_per_step": 4 * world},
+                     {"bound": "latency", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                      "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
+                      "note": "4 MiB collection: L2-resident and launch-latency bound (2 launches/step); no HBM claim"},
+                     cpu, {"workload": CONFIGS[0], "elements": n, "partitions": 4, "dtype": "f32", "fused": True})
+        pipe.close()
+    elif args.workload == "c3":
+        S, T = 1 << 34, 64
+        mine = shard_range(T, world, rank)
+        seeds = [42 + t for t in mine]
+        samples = [S // T + (1 if t < S % T else 0) for t in mine]
+        hits = torch.empty(max(1, len(seeds)), dtype=torch.int64, device=dev)
+        hits_host = torch.empty_like(hits, device="cpu").pin_memory()
+        fn = lambda: ops.pi_hits(seeds, samples, hits)
+        fn()
+        with B.ClockSampler(local) as clk:
+            l0 = capi.launch_count()
+            ms = _timed(fn, k, barrier)
+            launches = capi.launch_count() - l0
+
+        def e2e():
+            ops.pi_hits(seeds, samples, hits)
+            hits_host.copy_(hits, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_ms = _timed(e2e, k, barrier)
+        ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
+        total_hits = int(hits.sum().item())
+        if rank == 0 and world == 1:
+            r = _ref_workload(["--w", "pi", "--samples", str(1 << 28), "--tasks", "64", "--steps", "1", "--warmup", "0"])
+            cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "samples/s", "cores": r["threads"],
+                   "kind": "reference", "sample": "2^28 samples in 64 tasks (the C3 task shape, 1/64 of the samples)"}
+        ipc_peak = 148 * 4 * (clk.summary()["sm_mhz"] or 1965.0) * 1e6 / 1e9  # warp-instr/s (G), 4 schedulers/SM
+        instr_per_sample = 46.0  # SASS count of the k_pi inner loop (ALU 22, FMA 18, FP64 6)
+        achieved = (S / world) / (ms * 1e-3) * instr_per_sample / 32 / 1e9
+        line = _line(args, world, "c3", CONFIGS[2], S / (ms * 1e-3), "samples/s", ms, launches, clk,
+                     {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": 16 * T,
+                      "d2h_bytes_per_step": 8 * T},
+                     {"bound": "issue", "achieved": achieved, "peak": ipc_peak, "unit": "Gwarp-instr/s",
+                      "frac": achieved / ipc_peak, "traffic": 0, "note": "integer-ALU / issue bound; no HBM traffic"},
+                     cpu, {"workload": CONFIGS[2], "samples": S, "tasks": T, "dtype": "u64/f64->i64",
+                           "hits_this_rank": total_hits})
+    elif args.workload == "c4":
+        H = W = 16384
+        R = 256
+        nb = H // R
+        mine = shard_range(nb, world, rank)
+        ln = len(mine)
+        inp = torch.empty(max(1, ln) * (R + 2) * W, dtype=torch.uint8, device=dev)
+        ops.fill_bytes_(inp, 7)
+        out = torch.empty(max(1, ln) * R * W, dtype=torch.uint8, device=dev)
+        in_off = [b * (R + 2) * W for b in range(ln)]
+        out_off = [b * R * W for b in range(ln)]
+        fn = lambda: ops.sobel_bands(inp, in_off, out, out_off, [R] * ln, W)
+        fn()
+        with B.ClockSampler(local) as clk:
+            l0 = capi.launch_count()
+            ms = _timed(fn, k, barrier)
+            launches = capi.launch_count() - l0
+        host_in = torch.empty_like(inp, device="cpu").pin_memory()
+        host_out = torch.empty_like(out, device="cpu").pin_memory()
+
+        def e2e():
+            inp.copy_(host_in, non_blocking=True)
+            fn()
+            host_out.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_ms = _timed(e2e, k, barrier)
+        ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
+        if rank == 0 and world == 1:
+            r = _ref_workload(["--w", "sobel", "--height", "2048", "--width", str(W), "--rows", str(R), "--steps", "1",
+                               "--warmup", "0"])
+            cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "pixels/s", "cores": r["threads"],
+                   "kind": "reference", "sample": "2048x16384 (8 of the 64 bands)"}
+        algo = ln * ((R + 2) * W + R * W)
+        achieved = algo / (ms * 1e-3) / 1e9
+        line = _line(args, world, "c4", CONFIGS[3], H * W / (ms * 1e-3), "pixels/s", ms, launches, clk,
+                     {"value": H * W / (e2e_ms * 1e-3), "unit": "pixels/s",
+                      "h2d_bytes_per_step": nb * (R + 2) * W, "d2h_bytes_per_step": H * W},
+                     {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                      "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
+                      "algorithmic_bytes_per_launch": algo},
+                     cpu, {"workload": CONFIGS[3], "height": H, "width": W, "bands": nb, "rows_per_band": R,
+                           "dtype": "u8"})
+    elif args.workload == "c5":
+        n, P = 8192, 8
+        mine = shard_range(P, world, rank)
+        A = torch.empty(n, n, device=dev)
+        Bm = torch.empty(n, n, device=dev)
+        Cm = torch.empty(n, n, device=dev)
+        ops.fill_uniform_(A, 100)
+        ops.fill_uniform_(Bm, 101)
+        fn = lambda: [ops.gemm_tf32(A, Bm, Cm, n) for _ in mine]
+        fn()
+        with B.ClockSampler(local) as clk:
+            l0 = capi.launch_count()
+            ms = _timed(fn, k, barrier)
+            launches = capi.launch_count() - l0
+        torch.backends.cuda.matmul.allow_tf32 = True
+        for _ in range(3):  # cuBLAS handle / heuristics / workspace outside the timed region
+            torch.matmul(A, Bm)
+        cub = _timed(lambda: torch.matmul(A, Bm), k, barrier)
+        hA = torch.empty_like(A, device="cpu").pin_memory()
+        hC = torch.empty_like(Cm, device="cpu").pin_memory()
+
+        def e2e():
+            for _ in mine:
+                A.copy_(hA, non_blocking=True)
+                Bm.copy_(hA, non_blocking=True)
+                ops.gemm_tf32(A, Bm, Cm, n)
+                hC.copy_(Cm, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_ms = _timed(e2e, max(1, k // 4), barrier)
+        ms, cub, e2e_ms = _max_over_ranks([ms, cub, e2e_ms], world, dev)
+        flops = 2.0 * n ** 3 * P
+        if rank == 0 and world == 1:
+            r = _ref_workload(["--w", "matmul", "--n", "256", "--parts", "2", "--steps", "1", "--warmup", "0"])
+            cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "FLOP/s", "cores": r["threads"],
+                   "kind": "reference", "sample": "2 partitions at n=256 (the fp32 class-D run(); 8192^3 is infeasible on CPU)"}
+        per_gpu = 2.0 * n ** 3 / (ms * 1e-3 / max(1, len(mine))) / 1e12
+        peak = 2.0 * n ** 3 / (cub * 1e-3) / 1e12
+        line = _line(args, world, "c5", CONFIGS[4], flops / (ms * 1e-3), "FLOP/s", ms, launches, clk,
+                     {"value": flops / (e2e_ms * 1e-3), "unit": "FLOP/s",
+                      "h2d_bytes_per_step": P * 2 * n * n * 4, "d2h_bytes_per_step": P * n * n * 4},
+                     {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s", "frac": per_gpu / peak,
+                      "traffic": None, "peak_kind": "cuBLAS TF32 8192^3 measured in this run"},
+                     cpu, {"workload": CONFIGS[4], "n": n, "partitions": P, "dtype": "tf32 (fp32 in/out, fp32 accumulate)"})
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0

@@ -763,6 +763,82 @@ json run_golden() {
 
 // ---- bench -------------------------------------------------------------------
 
+// Bounded CPU samples of the other BASELINE configs through the reference
+// Engine + HostParallelExecutor:
+//   --w pi      --samples S --tasks T          (C3 shape, S scaled down)
+//   --w sobel   --height H --width W --rows R  (C4: bands of R rows, halos)
+//   --w matmul  --n N --parts P                (C5 shape at a small n)
+int run_bench_workload(int argc, char** argv) {
+  std::string w = "pi";
+  std::uint64_t samples = 1u << 26, tasks = 64, H = 2048, W = 16384, R = 256, n = 256, parts = 2;
+  unsigned threads = std::thread::hardware_concurrency();
+  int steps = 2, warmup = 1;
+  for (int i = 2; i + 1 < argc; i += 2) {
+    std::string k = argv[i], v = argv[i + 1];
+    if (k == "--w") w = v;
+    else if (k == "--samples") samples = std::stoull(v);
+    else if (k == "--tasks") tasks = std::stoull(v);
+    else if (k == "--height") H = std::stoull(v);
+    else if (k == "--width") W = std::stoull(v);
+    else if (k == "--rows") R = std::stoull(v);
+    else if (k == "--n") n = std::stoull(v);
+    else if (k == "--parts") parts = std::stoull(v);
+    else if (k == "--threads") threads = static_cast<unsigned>(std::stoul(v));
+    else if (k == "--steps") steps = std::stoi(v);
+    else if (k == "--warmup") warmup = std::stoi(v);
+  }
+  KernelRegistry reg = make_registry(W, n);
+  DirectDriver drv(reg, host_device(threads));
+  Engine eng(drv, reg);
+  Dataset d;
+  std::string kernel;
+  double units = 0;
+  bool partition = false;
+  if (w == "pi") {
+    std::vector<Element> es;
+    for (std::uint64_t t = 0; t < tasks; ++t)
+      es.push_back(Element::i64({static_cast<std::int64_t>(42 + t),
+                                 static_cast<std::int64_t>(samples / tasks + (t < samples % tasks ? 1 : 0))}));
+    d = create_dataset(std::move(es), tasks);
+    kernel = "pi";
+    units = double(samples);
+  } else if (w == "sobel") {
+    auto img = sobel_image(H, W, 7);
+    auto bands = sobel_bands(img, H, W, R);
+    std::vector<Element> es;
+    for (auto& b : bands) es.push_back(Element::bytes(b));
+    const std::size_t nb = es.size();
+    d = create_dataset(std::move(es), nb);
+    kernel = "sobel";
+    units = double(H) * double(W);
+    partition = true;
+  } else if (w == "matmul") {
+    std::vector<std::vector<float>> es(parts, std::vector<float>(2 * n * n));
+    for (std::size_t p = 0; p < parts; ++p)
+      for (std::size_t i = 0; i < es[p].size(); ++i) es[p][i] = 2.0f * uniform01(100 + p, i) - 1.0f;
+    d = f32_dataset(es, parts);
+    kernel = "matmul";
+    units = 2.0 * double(n) * double(n) * double(n) * double(parts);
+  } else {
+    throw Error("unknown workload " + w);
+  }
+  std::vector<double> times;
+  for (int s = 0; s < warmup + steps; ++s) {
+    auto t0 = std::chrono::steady_clock::now();
+    Dataset r = partition ? eng.map_cl_partition(d, kernel) : eng.map_cl(d, kernel);
+    auto t1 = std::chrono::steady_clock::now();
+    if (s >= warmup) times.push_back(std::chrono::duration<double>(t1 - t0).count());
+  }
+  json out;
+  out["workload"] = w;
+  out["units"] = units;
+  out["threads"] = threads;
+  out["executor"] = threads <= 1 ? "host-seq" : "host-par";
+  out["step_s"] = times;
+  std::cout << out.dump() << std::endl;
+  return 0;
+}
+
 int run_bench(int argc, char** argv) {
   std::size_t P = 4, L = 1u << 24;
   unsigned threads = std::thread::hardware_concurrency();
@@ -821,6 +897,7 @@ int main(int argc, char** argv) {
       return 0;
     }
     if (mode == "bench") return run_bench(argc, argv);
+    if (mode == "bench-workload") return run_bench_workload(argc, argv);
   } catch (const std::exception& e) {
     std::cerr << "ref_harness: " << e.what() << std::endl;
     return 1;
