@@ -176,10 +176,11 @@ def workload_config(args, world: int) -> dict:
         "elements": n, "partitions": args.parts, "part_len": args.part_len,
         "fused": not args.no_fuse,
         "fusion": "map+partition-reduce in one kernel, y materialised" if not args.no_fuse else "none",
-        "sharding": (f"partition blocks over {world} GPU(s); partials exchanged inside the finish kernel by "
-                     f"NVLink P2P stores + epoch flags (CUDA IPC), reference stage-2 tree on every rank"
-                     if world > 1 else "1 GPU: pass 1 + finish kernel (per-partition trees + stage-2 tree)"),
-        "steps_per_launch": "2 kernel launches per step",
+        "sharding": (f"partition blocks over {world} GPU(s); partials exchanged inside the reduction kernel's "
+                     f"tail by NVLink P2P stores + epoch flags (CUDA IPC), reference stage-2 tree on every rank"
+                     if world > 1 else "1 GPU: one kernel (stream + per-partition trees + stage-2 tree in its tail)"),
+        "steps_per_launch": ("1 kernel launch per step" if not args.no_fuse
+                             else "2 kernel launches per step (map, then reduce + trees)"),
         "l2": f"inputs larger than L2 ({n * 4 // world / 2**30:.2f} GiB x per GPU)",
     }
 
@@ -346,7 +347,7 @@ def our_arm(args, world, rank, local):
                     "d2h_bytes_per_step": 4 * world, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("ucg_map_affine_segment_reduce_f32 (pass1+pass2)" if not args.no_fuse
+                         "kernel": ("ucg_segment_reduce_cl_f32 (k_segment_pass1, trees in its tail)" if not args.no_fuse
                                     else "ucg_map_affine_f32 + ucg_segment_reduce_f32"),
                          "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": kern_ms,
                          "peak_kind": peak_kind, "frac_of_8TBs": achieved / 8000.0},

@@ -97,7 +97,7 @@ struct ucg_segtab {
   uint32_t* d_item_seg;    // [nitems]
   uint64_t max_items_per_seg;
   int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
-  uint32_t* d_done;        // finish-kernel CTA counter (zero between launches)
+  uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches)
 };
 
 // Peer-exchange context of a sharded reduce_cl (one process per GPU).

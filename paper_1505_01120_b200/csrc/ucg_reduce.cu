@@ -14,9 +14,11 @@
 // Operands are always combined as op(left, right) (std::max is not
 // commutative on signed zeros).
 //
-// Data movement: one warp owns a work item of 2^14 contiguous floats of one
-// segment and streams it in chunks of 128*U floats (U coalesced LDG.128 per
-// lane in flight). A chunk is reduced with a value-halving butterfly
+// Data movement: one warp owns a work item of 2^L contiguous floats of one
+// segment (L = 12 by default, ucg_segtab_create) and streams it in chunks of
+// 128*U floats (U coalesced LDG.128 per lane in flight, the next chunk's
+// loads issued before the current chunk is reduced). Warps claim items from
+// an atomic counter. A chunk is reduced with a value-halving butterfly
 // (U-1 + 5 shuffles per chunk instead of 5U).
 #include <cuda_runtime.h>
 
@@ -186,121 +188,73 @@ __device__ __forceinline__ float work_item(const float* __restrict__ x, float* _
   return v;
 }
 
-// Pass 1: one warp per work item (grid-stride over items). U = 4 keeps the
-// kernel under 40 registers so 6 CTAs (48 warps) stay resident per SM —
-// enough 16-byte loads in flight to cover HBM latency at full bandwidth.
-struct Pass1Args {
-  const float* x;
-  float* y;
-  const uint64_t* begin;
-  const uint64_t* len;
-  const uint64_t* first_item;
-  const uint32_t* item_seg;
-  uint64_t nitems;
-  int item_log2;
-  float a, b;
-  float* partial;
+// ---- trees over values in global memory ----------------------------------------
+
+constexpr int kTreeThreads = 256;  // == kWarps * 32: pass 1 CTAs run the trees too
+constexpr int kTreeBlock = 8 * kTreeThreads;
+
+struct TreeSmem {
+  float warp_root[kWarps];
+  float stk[64];
 };
 
-// Pass 1: one warp per work item (grid-stride over items); item roots go to
-// `partial`, pass 2 reduces each segment's roots. (Finishing segments inside
-// pass 1 with a last-warp-done counter was measured 5% slower: the release
-// fence after each item waits for that warp's 32-64 KB of y stores.)
-template <class Op, bool kMap, int U, int kMinBlocks>
-__global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const __grid_constant__ Pass1Args p) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
-  const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
-  for (uint64_t item = warp; item < p.nitems; item += nwarps) {
-    const uint32_t s = p.item_seg[item];
-    const uint64_t blk = item - p.first_item[s];
-    const uint64_t off = p.begin[s] + (blk << p.item_log2);
-    const int64_t item_floats = int64_t(1) << p.item_log2;
-    const int64_t valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
-    const float r = work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
-    if (lane == 0) p.partial[item] = r;
-  }
-}
-
-// Tree over n values in global memory by ONE CTA (blockDim 256), padded to a
-// power of two with the identity. Values are consumed in aligned blocks of
-// 2048 whose roots are merged with a binary-counter stack.
-constexpr int kTreeThreads = 256;
-constexpr int kTreeBlock = 2048;
-
+// Tree over n values (L2-resident item roots or partition values) by ONE CTA
+// of 256 threads, padded to a power of two with the identity. Values are
+// consumed in aligned blocks of 2048: thread t combines its 8 contiguous
+// values (3 tree levels in registers), the warp finishes 5 levels with xor
+// shuffles (lower lane = left operand), thread 0 the last 3 over the warp
+// roots — one barrier per block. Block roots are merged by a binary-counter
+// stack of aligned subtrees and the stack is folded right to left.
 template <class Op>
-__device__ float cta_tree(const float* __restrict__ vals, uint64_t n, float* sm /*kTreeBlock*/,
-                          float* stk /*64*/) {
-  const int tid = threadIdx.x;
+__device__ float cta_tree(const float* __restrict__ vals, uint64_t n, TreeSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint64_t nblocks = (n + kTreeBlock - 1) / kTreeBlock;
-  // one block of 2048 is the whole tree when n <= 2048 (padded size = pow2 >= n)
-  float root = Op::identity();
   for (uint64_t bi = 0; bi < nblocks; ++bi) {
-    const uint64_t base = bi * kTreeBlock;
-    const uint64_t cnt = umin(kTreeBlock, n - base);
-    // a partial block padded to any power of two >= cnt has the same root
-    int size = 1;
-    while (uint64_t(size) < cnt) size <<= 1;
-    for (int i = tid; i < size; i += kTreeThreads)
-      sm[i] = uint64_t(i) < cnt ? __ldcg(vals + base + i) : Op::identity();
+    const uint64_t base = bi * kTreeBlock + 8 * uint64_t(tid);
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = base + k < n ? __ldcg(vals + base + k) : Op::identity();
+    float r = Op::apply(Op::apply(Op::apply(v[0], v[1]), Op::apply(v[2], v[3])),
+                        Op::apply(Op::apply(v[4], v[5]), Op::apply(v[6], v[7])));
+#pragma unroll
+    for (int j = 0; j < 5; ++j) r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1 << j), !((lane >> j) & 1));
+    if (lane == 0) sm.warp_root[w] = r;
     __syncthreads();
-    for (int w = size / 2; w >= 1; w >>= 1) {
-      for (int i = tid; i < w; i += kTreeThreads) sm[i] = Op::apply(sm[2 * i], sm[2 * i + 1]);
-      __syncthreads();
-    }
     if (tid == 0) {
-      float v = sm[0];
+      const float* q = sm.warp_root;
+      float b = Op::apply(Op::apply(Op::apply(q[0], q[1]), Op::apply(q[2], q[3])),
+                          Op::apply(Op::apply(q[4], q[5]), Op::apply(q[6], q[7])));
       int j = 0;
-      // binary-counter merge of this block (index bi) into the stack
-      while ((bi >> j) & 1) {
-        v = Op::apply(stk[j], v);
+      while ((bi >> j) & 1) {  // binary-counter merge of block bi
+        b = Op::apply(sm.stk[j], b);
         ++j;
       }
-      stk[j] = v;
+      sm.stk[j] = b;
     }
     __syncthreads();
   }
+  float root = Op::identity();
   if (tid == 0 && nblocks) {
-    // fold the remaining stack right to left: smaller (right) subtrees first
     bool have = false;
-    float acc = Op::identity();
     for (int j = 0; j < 64; ++j) {
       if ((nblocks >> j) & 1) {
-        acc = have ? Op::apply(stk[j], acc) : stk[j];
+        root = have ? Op::apply(sm.stk[j], root) : sm.stk[j];
         have = true;
       }
     }
-    root = acc;
   }
   return root;  // valid in thread 0
 }
 
-// Pass 2: one CTA per segment; tree over the segment's work-item values.
-template <class Op>
-__global__ void __launch_bounds__(kTreeThreads)
-    k_segment_pass2(const float* __restrict__ partial, const uint64_t* __restrict__ first_item,
-                    float* __restrict__ out) {
-  __shared__ float sm[kTreeBlock];
-  __shared__ float stk[64];
-  const uint64_t s = blockIdx.x;
-  const uint64_t f = first_item[s], n = first_item[s + 1] - f;
-  if (n == 0) {
-    if (threadIdx.x == 0) out[s] = Op::empty();
-    return;
-  }
-  const float r = cta_tree<Op>(partial + f, n, sm, stk);
-  if (threadIdx.x == 0) out[s] = r;
-}
-
-// ---- pass 2 + reduce_cl stage 2 (+ the cross-GPU exchange) in one kernel -------
+// ---- partition values + reduce_cl stage 2 (+ the cross-GPU exchange) ---------------
 
 struct FinishArgs {
   const float* partial;       // item roots from pass 1
   const uint64_t* first_item;
   uint64_t nseg;
   float* out;                 // this rank's per-segment (partition) values
-  uint32_t* done;             // CTA-completion counter, reset by the last CTA
-  float* result;              // reduce_cl result (every rank gets it)
+  uint32_t* done;             // [3] pass-1 exit / finisher / item counters, zero between launches
+  float* result;              // reduce_cl result (every rank gets it), or null
   // sharded exchange (world > 1): region r = rank r's IPC-mapped buffer
   int world, rank;
   uint64_t part_offset;       // first global partition index of this rank
@@ -308,7 +262,7 @@ struct FinishArgs {
   const uint64_t* peers;      // [world] region base addresses (this rank's own at [rank])
   uint64_t flags_offset;      // byte offset of the [world] epoch flags inside a region
   uint32_t epoch;
-  uint32_t* err;              // set to 1 when a peer never arrives
+  uint32_t* err;              // set to 1 when a wait times out
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -319,35 +273,47 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
-// One CTA per segment reduces that segment's item roots (pass 2). The last
-// CTA to finish then runs reduce_cl stage 2: on one GPU directly over the
-// partition values; sharded, it first stores this rank's values into every
-// peer's region over NVLink (P2P stores), raises its epoch flag there
-// (release, system scope), waits for all ranks' flags in its own region
-// (acquire) and runs the same pairing tree over all P values in partition
-// order — the collective fused into the reduction kernel, no NCCL launch.
+// Partition values of segments j, j+F, j+2F, ... (one CTA = finisher j of F).
 template <class Op>
-__global__ void __launch_bounds__(kTreeThreads) k_segment_finish(const __grid_constant__ FinishArgs p) {
-  __shared__ float sm[kTreeBlock];
-  __shared__ float stk[64];
+__device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm) {
+  for (uint64_t s = j; s < p.nseg; s += F) {
+    const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
+    const float r = n ? cta_tree<Op>(p.partial + f, n, sm) : Op::empty();
+    if (threadIdx.x == 0) __stcg(p.out + s, r);
+  }
+}
+
+// Called by all F finisher CTAs after their segments are written. The last
+// one to arrive resets the counters and runs reduce_cl stage 2: on one GPU
+// directly over the partition values; sharded, it first stores this rank's
+// values into every peer's region over NVLink (P2P stores), raises its epoch
+// flag there (release, system scope), waits for all ranks' flags in its own
+// region (acquire) and runs the same pairing tree over all P values in
+// partition order — the collective fused into the reduction kernel.
+template <class Op>
+__device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
   __shared__ bool last;
   const int tid = threadIdx.x;
-  const uint64_t s = blockIdx.x;
-  if (s < p.nseg) {
-    const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
-    const float r = n ? cta_tree<Op>(p.partial + f, n, sm, stk) : Op::empty();
-    if (tid == 0) __stcg(p.out + s, r);
-  }
-  if (!p.result) return;
+  __syncthreads();
   if (tid == 0) {
     __threadfence();
-    last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    last = atomicAdd(p.done + 1, 1u) == F - 1;
   }
   __syncthreads();
   if (!last) return;
-  if (tid == 0) *p.done = 0;
+  if (tid == 0) {
+    p.done[0] = 0;
+    p.done[1] = 0;
+    p.done[2] = 0;
+  }
   __threadfence();
+  if (!p.result) return;
   const float* vals = p.out;
   uint64_t nvals = p.nseg;
   if (p.world > 1) {
@@ -374,19 +340,95 @@ __global__ void __launch_bounds__(kTreeThreads) k_segment_finish(const __grid_co
     vals = reinterpret_cast<const float*>(p.peers[p.rank]);
     nvals = p.p_total;
   }
-  const float root = nvals ? cta_tree<Op>(vals, nvals, sm, stk) : Op::empty();
+  const float root = nvals ? cta_tree<Op>(vals, nvals, sm) : Op::empty();
   if (tid == 0) *p.result = root;
+}
+
+// Pass 1: one warp per work item (grid-stride over items); item roots go to
+// `partial`. With `finish` set (a cooperative launch: every CTA resident),
+// the partition values and reduce_cl stage 2 run in the same kernel: each
+// CTA takes an exit ticket after its last item; the last F = min(G, nseg)
+// ticket holders wait until all G CTAs have exited the streaming loop, then
+// reduce one segment each, and the last of them runs stage 2. One fence per
+// CTA, no kernel boundary between the stream and the trees. (Finishing
+// segments with a per-item last-warp counter was measured 5% slower: the
+// fence after each item waits for that warp's 32-64 KB of y stores.)
+struct Pass1Args {
+  const float* x;
+  float* y;
+  const uint64_t* begin;
+  const uint64_t* len;
+  const uint64_t* first_item;
+  const uint32_t* item_seg;
+  uint64_t nitems;
+  int item_log2;
+  float a, b;
+  float* partial;
+  int finish;
+  int dynamic;  // claim items from the counter fin.done[2] instead of grid-stride
+  FinishArgs fin;
+};
+
+template <class Op, bool kMap, int U, int kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const __grid_constant__ Pass1Args p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
+  const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
+  uint64_t item = warp;
+  while (item < p.nitems) {
+    // dynamic: the next item index is claimed now and consumed after this one
+    uint32_t claim = 0;
+    if (p.dynamic && lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
+    const uint32_t s = p.item_seg[item];
+    const uint64_t blk = item - p.first_item[s];
+    const uint64_t off = p.begin[s] + (blk << p.item_log2);
+    const int64_t item_floats = int64_t(1) << p.item_log2;
+    const int64_t valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
+    const float r = work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
+    if (lane == 0) p.partial[item] = r;
+    item = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : item + nwarps;
+  }
+  if (!p.finish) return;
+  __shared__ TreeSmem sm;
+  __shared__ uint32_t ticket;
+  const uint32_t G = gridDim.x;
+  const uint32_t F = uint32_t(umin(G, p.fin.nseg ? p.fin.nseg : 1));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    ticket = atomicAdd(p.fin.done, 1u);
+  }
+  __syncthreads();
+  if (ticket + F < G) return;
+  if (threadIdx.x == 0) {
+    uint64_t spins = 0;
+    while (ld_acquire_gpu(p.fin.done) < G) {
+      __nanosleep(32);
+      if (++spins > (1ull << 25)) {  // cannot happen under a cooperative launch
+        if (p.fin.err) atomicExch(p.fin.err, 2u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  segment_values<Op>(p.fin, ticket + F - G, F, sm);
+  stage2<Op>(p.fin, F, sm);
+}
+
+// Stand-alone finish (tables with no work items, or UCG_SEPARATE_FINISH=1):
+// one CTA per segment, then stage 2 by the last CTA.
+template <class Op>
+__global__ void __launch_bounds__(kTreeThreads) k_segment_finish(const __grid_constant__ FinishArgs p) {
+  __shared__ TreeSmem sm;
+  const uint32_t F = gridDim.x;
+  if (blockIdx.x < p.nseg) segment_values<Op>(p, blockIdx.x, F, sm);
+  stage2<Op>(p, F, sm);
 }
 
 template <class Op>
 __global__ void __launch_bounds__(kTreeThreads) k_tree(const float* __restrict__ x, uint64_t n, float* __restrict__ out) {
-  __shared__ float sm[kTreeBlock];
-  __shared__ float stk[64];
-  if (n == 0) {
-    if (threadIdx.x == 0) out[0] = Op::empty();
-    return;
-  }
-  const float r = cta_tree<Op>(x, n, sm, stk);
+  __shared__ TreeSmem sm;
+  const float r = n ? cta_tree<Op>(x, n, sm) : Op::empty();
   if (threadIdx.x == 0) out[0] = r;
 }
 
@@ -503,33 +545,60 @@ inline int pass1_variant() {
 }
 
 template <class Op, bool kMap, int U, int MINB>
-void launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_t st) {
+cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_t st) {
   const uint64_t want = (t->nitems + kWarps - 1) / kWarps;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sm_count()) * MINB)));
-  k_segment_pass1<Op, kMap, U, MINB><<<grid, kWarps * 32, 0, st>>>(args);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kWarps * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = args.finish ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, args);
 }
 
 template <class Op, bool kMap>
-void dispatch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_t st) {
+cudaError_t dispatch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_t st) {
   switch (pass1_variant()) {
-    case 1: launch_pass1<Op, kMap, 4, 3>(args, t, st); break;
-    case 2: launch_pass1<Op, kMap, 4, 4>(args, t, st); break;
-    case 3: launch_pass1<Op, kMap, 2, 8>(args, t, st); break;
-    case 4: launch_pass1<Op, kMap, 2, 6>(args, t, st); break;
-    case 5: launch_pass1<Op, kMap, 8, 3>(args, t, st); break;
-    default: launch_pass1<Op, kMap, 8, 2>(args, t, st); break;
+    case 1: return launch_pass1<Op, kMap, 4, 3>(args, t, st);
+    case 2: return launch_pass1<Op, kMap, 4, 4>(args, t, st);
+    case 3: return launch_pass1<Op, kMap, 2, 8>(args, t, st);
+    case 4: return launch_pass1<Op, kMap, 2, 6>(args, t, st);
+    case 5: return launch_pass1<Op, kMap, 8, 3>(args, t, st);
+    default: return launch_pass1<Op, kMap, 8, 2>(args, t, st);
   }
 }
 
+// Items are claimed dynamically by default (UCG_DYNAMIC_ITEMS=0: grid-stride).
+// Measured on B200 (tools/scaling_probe.py, ncu dram__throughput): 2^30 fp32
+// fused map+psum 1.266 ms / 82.4% of DRAM peak claimed vs 1.380 ms / 75.6%
+// grid-stride — warps stay on one compact, advancing address window instead
+// of drifting apart, and the last items balance across SMs.
+inline bool dynamic_items() {
+  static const bool v = [] {
+    const char* e = getenv("UCG_DYNAMIC_ITEMS");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+
+inline bool separate_finish() {
+  static const bool v = [] {
+    const char* e = getenv("UCG_SEPARATE_FINISH");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
+// Pass 1 with the partition trees and reduce_cl stage 2 folded into its tail
+// (one launch per step); a table without work items launches the stand-alone
+// finish kernel instead.
 template <class Op>
 int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, float* out,
                    float* result, ucg_xchg* xg, cudaStream_t st) {
-  Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2, a, b, scratch};
-  if (t->nitems) {
-    if (y) dispatch_pass1<Op, true>(args, t, st);
-    else dispatch_pass1<Op, false>(args, t, st);
-    UCG_LAUNCHED();
-  }
   FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr};
   if (xg) {
     f.world = xg->world;
@@ -541,7 +610,15 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.epoch = ++xg->epoch;
     f.err = xg->d_err;
   }
-  if (t->nseg || result) {
+  const bool fused_finish = t->nitems && !separate_finish();
+  if (t->nitems) {
+    Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
+                   a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, f};
+    const cudaError_t e = y ? dispatch_pass1<Op, true>(args, t, st) : dispatch_pass1<Op, false>(args, t, st);
+    UCG_CUDA(e);
+    UCG_LAUNCHED();
+  }
+  if (!fused_finish && (t->nseg || result)) {
     k_segment_finish<Op><<<unsigned(std::max<uint64_t>(1, t->nseg)), kTreeThreads, 0, st>>>(f);
     UCG_LAUNCHED();
   }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -251,27 +252,17 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if (int rc = check_device()) return rc;
   if (nseg && (!begin || !len)) return fail(UCG_ERR_ARG, "begin/len is null");
   if (nseg >= (1ull << 32)) return fail(UCG_ERR_ARG, "too many segments");
-  // work-item size: the largest 2^L (L in [11,14]) whose item count fills the
-  // last wave of resident warps to >= 95% (else the best-filled one)
-  uint64_t total = 0;
-  for (uint64_t s = 0; s < nseg; ++s) total += len[s];
-  const uint64_t warps = uint64_t(sm_count()) * 16;
-  int item_log2 = kMaxItemLog2;
-  double best = -1.0;
-  for (int L = kMaxItemLog2; L >= kMinItemLog2; --L) {
-    uint64_t items = 0;
-    for (uint64_t s = 0; s < nseg; ++s) items += (len[s] + (1ull << L) - 1) >> L;
-    const double fill = items ? double(items) / double((items + warps - 1) / warps * warps) : 1.0;
-    if (fill > best + 1e-9) {
-      best = fill;
-      item_log2 = L;
-    }
-    if (fill >= 0.95) {
-      item_log2 = L;
-      break;
-    }
+  // work-item size: 2^12 floats (16 KB; items are claimed dynamically, so
+  // no wave quantisation to fit), 2^11 when that leaves fewer items than
+  // resident warps. Sweep: tools/scaling_probe.py (2^12 best from 2^27 to
+  // 2^30 elements; 2^11 restarts the load pipeline too often).
+  uint64_t items12 = 0;
+  for (uint64_t s = 0; s < nseg; ++s) items12 += (len[s] + 4095) >> 12;
+  int item_log2 = items12 < uint64_t(sm_count()) * 16 ? kMinItemLog2 : 12;
+  if (const char* e = getenv("UCG_ITEM_LOG2")) {  // tuning override (tools/)
+    const int L = atoi(e);
+    if (L >= kMinItemLog2 && L <= kMaxItemLog2) item_log2 = L;
   }
-  (void)total;
   std::vector<uint64_t> first(nseg + 1, 0);
   uint64_t maxi = 0;
   for (uint64_t s = 0; s < nseg; ++s) {
@@ -304,8 +295,8 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if ((e = cudaMalloc(&t->d_len, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_first_item, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMalloc(&t->d_done, 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMemset(t->d_done, 0, 4)) != cudaSuccess) return cleanup(e, "cudaMemset");
+  if ((e = cudaMalloc(&t->d_done, 16)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMemset(t->d_done, 0, 16)) != cudaSuccess) return cleanup(e, "cudaMemset");
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");

@@ -95,6 +95,75 @@ def test_fused_map_reduce_bitexact(cuda, op):
     tab.close()
 
 
+def _special_segments(lens, seed):
+    """Segments mixing NaN payloads, +-inf, +-0, subnormals and values large
+    enough that partial sums overflow — the tree ORDER decides every result
+    (std::max keeps the left operand on NaN; inf + -inf appears mid-tree)."""
+    from paper_1505_01120_b200.pipeline import Layout
+
+    rng = np.random.default_rng(seed)
+    lay = Layout.of(lens)
+    buf = np.zeros(lay.total, np.float32)
+    host = []
+    pool = np.array([np.inf, -np.inf, 0.0, -0.0, 1e-40, -3e-39, 3e38, -3e38, 1.5, -2.25],
+                    np.float32)
+    nans = np.array([0x7fc00000, 0xffc00001, 0x7fa00000, 0x7f800001], np.uint32).view(np.float32)
+    for k, n in enumerate(lens):
+        v = (rng.standard_normal(n) * 1e3).astype(np.float32)
+        m = rng.random(n)
+        dens = [0.0, 1e-4, 0.01, 0.2][k % 4]
+        sel = m < dens
+        v[sel] = pool[rng.integers(0, pool.size, sel.sum())]
+        if k % 3 == 1 and n:
+            nsel = m > 1.0 - dens / 4
+            v[nsel] = nans[rng.integers(0, nans.size, nsel.sum())]
+        if k == 5:
+            v[0] = nans[1]  # leftmost NaN stays the left operand up the whole tree
+        buf[lay.begins[k]: lay.begins[k] + n] = v
+        host.append(v)
+    return lay, buf, host
+
+
+def _same_float(got: np.ndarray, want: np.ndarray, op: str) -> bool:
+    """Bit equality; for sums a NaN result only needs to be a NaN (x86 keeps
+    the first operand's payload, the GPU returns the canonical NaN). max
+    returns one operand unchanged, so its NaN payloads must match exactly."""
+    if op == "max":
+        return np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    both_nan = np.isnan(got) & np.isnan(want)
+    return bool(np.all(both_nan | (got.view(np.uint32) == want.view(np.uint32))))
+
+
+@pytest.mark.parametrize("op", ["sum", "max"])
+@pytest.mark.parametrize("fused", [False, True])
+def test_segment_reduce_special_values(cuda, op, fused):
+    from paper_1505_01120_b200 import capi, ops
+
+    lens = [1, 2, 3, 1025, 4096, 16385, 65536, 100003, 0, 262144, 333333, 7]
+    lay, buf, host = _special_segments(lens, seed=23)
+    x = torch.from_numpy(buf).to(cuda)
+    tab = capi.SegTab(lay.begins, lens)
+    scratch = torch.empty(tab.scratch_floats, dtype=torch.float32, device=cuda)
+    out = torch.empty(len(lens), dtype=torch.float32, device=cuda)
+    if fused:
+        y = torch.empty_like(x)
+        ops.map_affine_segment_reduce(x, y, tab, 2.0, -1.0, op, scratch, out)
+        want = np.array([O.tree_reduce(O.map_affine(h, 2.0, -1.0), op) for h in host], np.float32)
+        yh = y.cpu().numpy()
+        for k, h in enumerate(host):
+            got_y = yh[lay.begins[k]: lay.begins[k] + len(h)]
+            assert _same_float(got_y, O.map_affine(h, 2.0, -1.0), "sum")
+    else:
+        ops.segment_reduce(x, tab, op, scratch, out)
+        want = np.array([O.tree_reduce(h, op) for h in host], np.float32)
+    got = out.cpu().numpy()
+    assert np.isnan(want).any() and np.isinf(want).any() if op == "max" else np.isnan(want).any()
+    # after the map every NaN is the device's canonical NaN (fl(a*NaN) payload
+    # is hardware-defined), so only the unmapped max keeps payloads bit-exact
+    assert _same_float(got, want, "sum" if fused else op), (got, want)
+    tab.close()
+
+
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 7, 64, 1000, 2048, 2049, 5000, 70001])
 @pytest.mark.parametrize("op", ["sum", "max"])
 def test_tree_reduce_bitexact(cuda, n, op):
