@@ -187,6 +187,7 @@ struct SobelTiles {
   uint32_t first_tile[kMaxBands + 1];
   uint32_t nbands;
   uint32_t col_tiles;
+  uint32_t mul[3];  // {1, 2, 0xFFFFFFFF} (see k_sobel_tma)
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -266,31 +267,44 @@ __global__ void __launch_bounds__(kTmaThreads)
     const uint8_t* right = left + kSideStride;
     // smem reads through explicit shared-window addresses (LDS, not generic LD)
     const uint32_t c_s = sa(center), l_s = sa(left), r_s = sa(right);
+    // multipliers opaque to the compiler (kernel parameters): x*k+y stays an
+    // IMAD on the FMA pipe instead of becoming an IADD3/LEA on the ALU pipe
+    const uint32_t one = p.mul[0], two = p.mul[1], m1 = p.mul[2];
+    // Row terms in even/odd planes: for word k (pixels 4k..4k+3) the even
+    // plane holds pixels (4k, 4k+2) and the odd plane (4k+1, 4k+3) as 16-bit
+    // halves, so the right neighbours of even pixels ARE the odd plane and
+    // the left neighbours of odd pixels ARE the even plane; only the other
+    // two neighbour vectors need one byte permute each (4 PRMT per 4 pixels
+    // instead of 8). Terms are left unbiased: every linear step is exact
+    // mod 2^32 on the packed word (a negative low half borrows from the high
+    // half consistently), and emit adds the bias that makes both halves
+    // non-negative before the per-half min/max.
     auto terms = [&](int i, RowTerms& tr) {
       const uint32_t row = c_s + uint32_t(i * kTW + cg * 16);
       uint4 w;
-      uint32_t lft, rgt;
+      uint32_t pw, nw;
       asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(row));
-      const uint32_t la = cg ? row - 1 : l_s + uint32_t(i * 16 + 15);
-      const uint32_t ra = cg < 15 ? row + 16 : r_s + uint32_t(i * 16);
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(lft) : "r"(la));
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(rgt) : "r"(ra));
-      const uint32_t ws[6] = {lft << 24, w.x, w.y, w.z, w.w, rgt};
+      // the 4-byte words holding pixel -1 (byte 3) and pixel 16 (byte 0)
+      const uint32_t pa = cg ? row - 4 : l_s + uint32_t(i * 16 + 12);
+      const uint32_t na = cg < 15 ? row + 16 : r_s + uint32_t(i * 16);
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw) : "r"(na));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      uint32_t E[4], O[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint32_t cur = ws[k + 1];
-        const uint32_t sl = __byte_perm(ws[k], cur, 0x6543);
-        const uint32_t sr = __byte_perm(cur, ws[k + 2], 0x4321);
+        E[k] = __byte_perm(ws[k], 0, 0x4240);  // (p[4k], p[4k+2])
+        O[k] = __byte_perm(ws[k], 0, 0x4341);  // (p[4k+1], p[4k+3])
+      }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t sel = h ? 0x4342u : 0x4140u;
-          // E, L: bytes -> 16-bit halves; Rb = R + 256 per half (the 0x01 filler bytes)
-          const uint32_t E = __byte_perm(cur, 0, sel), L = __byte_perm(sl, 0, sel);
-          const uint32_t Rb = __byte_perm(sr, 0x01010101u, sel);
-          // half the adds on the FMA pipe (IMAD), the byte permutes/min/max on the ALU pipe
-          tr.dh[2 * k + h] = mad_u32(L, 0xFFFFFFFFu, Rb);       // R - L + 256
-          tr.sh[2 * k + h] = mad_u32(E, 2u, L + Rb);            // L + 2E + R + 256
-        }
+      for (int k = 0; k < 4; ++k) {
+        // left of the even pixels (p[4k-1], p[4k+1]); right of the odd ones (p[4k+2], p[4k+4])
+        const uint32_t Le = k ? __byte_perm(O[k - 1], O[k], 0x5432) : __byte_perm(pw, O[0], 0x5453);
+        const uint32_t Ro = k < 3 ? __byte_perm(E[k], E[k + 1], 0x5432) : __byte_perm(E[3], nw, 0x1432);
+        tr.dh[2 * k] = mad_u32(Le, m1, O[k]);                 // R - L, even
+        tr.dh[2 * k + 1] = mad_u32(E[k], m1, Ro);             // R - L, odd
+        tr.sh[2 * k] = mad_u32(E[k], two, mad_u32(Le, one, O[k]));      // L + 2C + R, even
+        tr.sh[2 * k + 1] = mad_u32(O[k], two, mad_u32(E[k], one, Ro));  // L + 2C + R, odd
       }
     };
     uint8_t* dst = out + p.out_off[b] + (uint64_t(rb) * kTH + rg * 8) * width + col;
@@ -299,14 +313,15 @@ __global__ void __launch_bounds__(kTmaThreads)
       uint32_t o[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const uint32_t gx = mad_u32(bb.dh[i], 2u, a.dh[i] + c.dh[i]);   // Gx + 1024
-        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;             // Gy + 1024
-        const uint32_t ax = __vmaxu2(gx, mad_u32(gx, 0xFFFFFFFFu, 0x08000800u));
-        const uint32_t ay = __vmaxu2(gy, mad_u32(gy, 0xFFFFFFFFu, 0x08000800u));
-        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);
+        const uint32_t gx = mad_u32(bb.dh[i], two, a.dh[i] + c.dh[i] + 0x04000400u);  // Gx + 1024 per half
+        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;                            // Gy + 1024 per half
+        const uint32_t ax = __vmaxu2(gx, mad_u32(gx, m1, 0x08000800u));
+        const uint32_t ay = __vmaxu2(gy, mad_u32(gy, m1, 0x08000800u));
+        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);  // min(|Gx|+|Gy|, 255) + 2048
       }
-      const uint32_t q0 = __byte_perm(o[0], o[1], 0x6420), q1 = __byte_perm(o[2], o[3], 0x6420);
-      const uint32_t q2 = __byte_perm(o[4], o[5], 0x6420), q3 = __byte_perm(o[6], o[7], 0x6420);
+      // interleave the planes back: bytes (even lo, odd lo, even hi, odd hi)
+      const uint32_t q0 = __byte_perm(o[0], o[1], 0x6240), q1 = __byte_perm(o[2], o[3], 0x6240);
+      const uint32_t q2 = __byte_perm(o[4], o[5], 0x6240), q3 = __byte_perm(o[6], o[7], 0x6240);
       st_stream(reinterpret_cast<float4*>(dst + uint64_t(r) * width),
                 make_float4(__uint_as_float(q0), __uint_as_float(q1), __uint_as_float(q2), __uint_as_float(q3)));
     };
@@ -411,6 +426,9 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       SobelTiles p;
       p.nbands = nb;
       p.col_tiles = col_tiles;
+      p.mul[0] = 1;
+      p.mul[1] = 2;
+      p.mul[2] = 0xFFFFFFFFu;
       p.first_tile[0] = 0;
       for (uint32_t i = 0; i < nb; ++i) {
         p.in_row0[i] = uint32_t(in_off[b0 + i] / width);
