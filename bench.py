@@ -33,6 +33,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# stdout carries exactly one JSON line: NCCL's banner / INFO log goes to stderr
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "mapCL+reduceCL elements/sec and % HBM roofline at 1/2/4/8 B200 vs host CPU"
 UNIT = "elements/s"
