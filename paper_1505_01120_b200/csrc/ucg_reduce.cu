@@ -263,6 +263,7 @@ struct FinishArgs {
   uint64_t flags_offset;      // byte offset of the [world] epoch flags inside a region
   uint32_t epoch;
   uint32_t* err;              // set to 1 when a wait times out
+  int warp_mode;              // one warp (not one CTA) per segment
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -279,9 +280,53 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   return v;
 }
 
-// Partition values of segments j, j+F, j+2F, ... (one CTA = finisher j of F).
+// Tree over n <= 2^13 values by ONE warp: blocks of 256 (lane l combines its
+// 8 contiguous values, 5 xor-shuffle levels finish the block), block roots
+// merged by a register binary-counter stack, folded right to left.
+constexpr int kWarpTreeDepth = 5;  // up to 32 blocks
+template <class Op>
+__device__ float warp_tree(const float* __restrict__ vals, uint64_t n, int lane) {
+  const uint32_t nb = uint32_t((n + 255) / 256);
+  float stk[kWarpTreeDepth];
+#pragma unroll
+  for (int j = 0; j < kWarpTreeDepth; ++j) stk[j] = Op::identity();
+#pragma unroll 1
+  for (uint32_t c = 0; c < nb; ++c) {
+    const uint64_t base = uint64_t(c) * 256 + 8 * lane;
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = base + k < n ? __ldcg(vals + base + k) : Op::identity();
+    float r = Op::apply(Op::apply(Op::apply(v[0], v[1]), Op::apply(v[2], v[3])),
+                        Op::apply(Op::apply(v[4], v[5]), Op::apply(v[6], v[7])));
+#pragma unroll
+    for (int j = 0; j < 5; ++j) r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1 << j), !((lane >> j) & 1));
+    counter_push<Op, kWarpTreeDepth>(stk, r, int(c));
+  }
+  bool have = false;
+  float root = Op::identity();
+#pragma unroll
+  for (int j = 0; j < kWarpTreeDepth; ++j) {
+    if ((nb >> j) & 1) {
+      root = have ? Op::apply(stk[j], root) : stk[j];
+      have = true;
+    }
+  }
+  return root;
+}
+
+// Partition values of segments j, j+F, j+2F, ... (one CTA = finisher j of F),
+// or — with many partitions of few items (warp_mode) — one warp per segment.
 template <class Op>
 __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm) {
+  if (p.warp_mode) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t s = j * kWarps + (threadIdx.x >> 5); s < p.nseg; s += F * kWarps) {
+      const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
+      const float r = n ? warp_tree<Op>(p.partial + f, n, lane) : Op::empty();
+      if (lane == 0) __stcg(p.out + s, r);
+    }
+    return;
+  }
   for (uint64_t s = j; s < p.nseg; s += F) {
     const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
     const float r = n ? cta_tree<Op>(p.partial + f, n, sm) : Op::empty();
@@ -599,7 +644,7 @@ inline bool separate_finish() {
 template <class Op>
 int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, float* out,
                    float* result, ucg_xchg* xg, cudaStream_t st) {
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr};
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -611,6 +656,10 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.err = xg->d_err;
   }
   const bool fused_finish = t->nitems && !separate_finish();
+  // many partitions of few items: a warp per partition tree (the fused tail
+  // has only min(G, P) finisher CTAs; G = 2 CTAs per SM)
+  f.warp_mode = fused_finish && t->nseg > uint64_t(sm_count()) * 4 &&
+                t->max_items_per_seg <= (uint64_t(256) << kWarpTreeDepth);
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
                    a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, f};

@@ -72,7 +72,7 @@ def map_affine_segment_reduce(x, y, segtab: capi.SegTab, a: float, b: float, op:
 
 def segment_reduce_cl(x, y, segtab: capi.SegTab, a: float, b: float, op: str, scratch, partials, xchg, result,
                       stream=None):
-    """map_cl(axpb) (when y is given) -> map_cl_partition(p<op>) -> reduce_cl(<op>2) in two launches;
+    """map_cl(axpb) (when y is given) -> map_cl_partition(p<op>) -> reduce_cl(<op>2) in one launch;
     xchg (a ucg_xchg handle) makes the last stage a fused cross-GPU exchange."""
     _require_cuda(x, scratch, partials, result)
     call("ucg_segment_reduce_cl_f32", ptr(x), ptr(y), segtab.handle, a, b, capi.OPS[op], ptr(scratch), ptr(partials),

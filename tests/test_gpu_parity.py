@@ -164,6 +164,33 @@ def test_segment_reduce_special_values(cuda, op, fused):
     tab.close()
 
 
+@pytest.mark.parametrize("op", ["sum", "max"])
+@pytest.mark.parametrize("fused", [False, True])
+def test_many_partitions_bitexact(cuda, op, fused):
+    """More partitions than finisher CTAs (one warp per partition tree in the
+    kernel tail), empty and ragged ones included, through reduce_cl."""
+    from paper_1505_01120_b200 import capi, ops
+
+    rng = np.random.default_rng(31)
+    lens = [int(v) for v in rng.integers(0, 20000, 2500)]
+    lens[7] = 0
+    lens[100] = 1
+    lay, buf, host = _segments(lens, seed=41)
+    x = torch.from_numpy(buf).to(cuda)
+    y = torch.empty_like(x) if fused else None
+    tab = capi.SegTab(lay.begins, lens)
+    scratch = torch.empty(tab.scratch_floats, dtype=torch.float32, device=cuda)
+    parts = torch.empty(len(lens), dtype=torch.float32, device=cuda)
+    res = torch.empty(1, dtype=torch.float32, device=cuda)
+    for _ in range(2):  # the table's counters must be reusable launch after launch
+        ops.segment_reduce_cl(x, y, tab, 2.0, 1.0, op, scratch, parts, None, res)
+    vals = [O.map_affine(h, 2.0, 1.0) if fused else h for h in host]
+    want = np.array([O.tree_reduce(v, op) for v in vals], np.float32)
+    assert np.array_equal(_bits(parts), want.view(np.uint32))
+    assert _bits(res)[0] == np.float32(O.tree_reduce(want, op)).view(np.uint32)
+    tab.close()
+
+
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 7, 64, 1000, 2048, 2049, 5000, 70001])
 @pytest.mark.parametrize("op", ["sum", "max"])
 def test_tree_reduce_bitexact(cuda, n, op):
