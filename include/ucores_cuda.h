@@ -69,6 +69,8 @@ typedef struct ucg_device_info {
 } ucg_device_info;
 int ucg_device_info_get(int ordinal, ucg_device_info* out);
 int ucg_set_device(int ordinal);
+/** The calling thread's current device (cudaGetDevice). */
+int ucg_get_device(int* ordinal_out);
 
 /* Device / pinned-host memory and copies (the partition upload path; replaces
  * the host copies at ucores/kernel.hpp:103-112 bind and :137-147 take). */

@@ -37,6 +37,7 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_device_count": (i32, [P(C.c_int)]),
     "ucg_device_info_get": (i32, [C.c_int, P(DeviceInfo)]),
     "ucg_set_device": (i32, [C.c_int]),
+    "ucg_get_device": (i32, [C.POINTER(C.c_int)]),
     "ucg_malloc": (i32, [P(vp), u64]),
     "ucg_free": (i32, [vp]),
     "ucg_host_alloc": (i32, [P(vp), u64]),

@@ -26,6 +26,16 @@ int check_device();  // UCG_OK when the current device is compute capability 10.
 int sm_count();      // SMs of the current device (cached per device)
 extern std::atomic<uint64_t> g_launches;
 
+// True the first time it is called on the current device for this flag word.
+// Kernel attributes (cudaFuncSetAttribute) are per device: a process driving
+// several GPUs (the seam-A driver) must set them on each one.
+inline bool first_on_device(std::atomic<uint64_t>& seen) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const uint64_t bit = 1ull << (d & 63);
+  return !(seen.fetch_or(bit) & bit);
+}
+
 #define UCG_CUDA(call)                                  \
   do {                                                  \
     cudaError_t _e = (call);                            \

@@ -525,21 +525,16 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
     const char* e = getenv("UCG_GEMM_VARIANT");
     return e ? atoi(e) : 2;  // default: CTA-pair (cta_group::2) kernel
   }();
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr = true;
+    UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
   }
   if (variant == 0) {
     dim3 grid(unsigned(n / BN), unsigned(n / BM));
     k_gemm_tf32<<<grid, 128, SMEM_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
   } else if (variant == 2) {
-    static bool attr2 = false;
-    if (!attr2) {
-      UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
-      attr2 = true;
-    }
     const uint64_t ntiles = (n / 256) * (n / 256);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count() / 2))) * 2;
     k_gemm_tf32_2sm<<<grid, 192, SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));

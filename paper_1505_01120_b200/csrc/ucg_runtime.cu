@@ -129,6 +129,11 @@ int ucg_set_device(int ordinal) {
   UCG_CUDA(cudaSetDevice(ordinal));
   return UCG_OK;
 }
+int ucg_get_device(int* ordinal_out) {
+  if (!ordinal_out) return fail(UCG_ERR_ARG, "ordinal_out is null");
+  UCG_CUDA(cudaGetDevice(ordinal_out));
+  return UCG_OK;
+}
 
 int ucg_malloc(void** dptr, uint64_t bytes) {
   if (!dptr) return fail(UCG_ERR_ARG, "dptr is null");

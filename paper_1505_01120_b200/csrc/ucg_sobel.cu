@@ -415,11 +415,9 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) return fail(UCG_ERR_CUDA, "sobel tensor map encode failed");
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr))
       UCG_CUDA(cudaFuncSetAttribute(k_sobel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * kBufBytes + 128)));
-      attr = true;
-    }
     const uint32_t col_tiles = uint32_t((width + kTW - 1) / kTW);
     for (uint64_t b0 = 0; b0 < nbands; b0 += kMaxBands) {
       const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));

@@ -65,6 +65,7 @@ class CudaExecutor : public ucores::KernelExecutor {
     }
     if (ctx.range().global_size == 0) return;
     std::lock_guard<std::mutex> lock(gpu_->mutex());
+    DeviceGuard guard;
     gpu_->bind();
     op->run_phase(*gpu_, ctx);
   }

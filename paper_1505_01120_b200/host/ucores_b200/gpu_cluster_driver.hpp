@@ -101,6 +101,7 @@ class GpuClusterDriver : public ucores::ClusterDriver {
     Gpu& gpu = *gpus_[g];
     auto attempt = [&](std::span<const ucores::Task* const> b) {
       std::lock_guard<std::mutex> lock(gpu.mutex());
+      DeviceGuard guard;
       gpu.bind();
       return op.run_tasks(gpu, b);
     };

@@ -63,11 +63,31 @@ class DeviceBuffer {
   std::uint64_t bytes_ = 0;
 };
 
+/// Restores the calling thread's current device on scope exit, so binding a
+/// Gpu never changes the device a caller (e.g. torch on the same thread)
+/// launches on afterwards.
+class DeviceGuard {
+ public:
+  DeviceGuard() {
+    if (ucg_get_device(&prev_) != UCG_OK) prev_ = -1;
+  }
+  ~DeviceGuard() {
+    if (prev_ >= 0) ucg_set_device(prev_);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+
+ private:
+  int prev_ = -1;
+};
+
 /// One B200: its ordinal, a non-blocking stream and reusable scratch. All
-/// calls made through a Gpu first bind its device on the calling thread.
+/// calls made through a Gpu first bind its device on the calling thread
+/// (under a DeviceGuard at every call site).
 class Gpu {
  public:
   explicit Gpu(int ordinal) : ordinal_(ordinal) {
+    DeviceGuard guard;
     bind();
     check(ucg_stream_create(&stream_), "run");
   }
@@ -75,6 +95,7 @@ class Gpu {
   Gpu& operator=(const Gpu&) = delete;
   ~Gpu() {
     if (stream_) {
+      DeviceGuard guard;
       ucg_set_device(ordinal_);
       ucg_stream_destroy(stream_);
     }
