@@ -298,6 +298,14 @@ def our_arm(args, world, rank, local):
     e2e_ms = te0.elapsed_time(te1) / args.e2e_steps
     wall_e2e_ms = (time.perf_counter() - e0) * 1e3 / args.e2e_steps
     h2d = pipe.h2d_bytes
+    # the e2e roofline: one plain pinned host->device copy of the same bytes
+    hc0, hc1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hc0.record()
+    pipe.x.copy_(pipe.host_x, non_blocking=True)
+    hc1.record()
+    hc1.synchronize()
+    h2d_gbs = pipe.host_x.numel() * 4 / (hc0.elapsed_time(hc1) * 1e-3) / 1e9
+    e2e_gbs = h2d / (e2e_ms * 1e-3) / 1e9
     if world > 1:
         import torch.distributed as dist
 
@@ -358,7 +366,9 @@ def our_arm(args, world, rank, local):
             "dtype": "f32", "data": "synthetic (counter-hash U[0,1), partition p seeded 1000+p, planted max)",
             "config": workload_config(args, world),
             "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 4 * world, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e_ms},
+                    "d2h_bytes_per_step": 4 * world, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_e2e_ms,
+                    "bound": "pcie", "h2d_gbs_per_gpu": e2e_gbs / world,
+                    "plain_h2d_copy_gbs_per_gpu": h2d_gbs, "frac_of_plain_copy": e2e_gbs / world / h2d_gbs},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": ("ucg_segment_reduce_cl_f32 (k_segment_pass1, trees in its tail)" if not args.no_fuse
