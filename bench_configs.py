@@ -109,7 +109,7 @@ def run(args, world, rank, local):
                       "d2h_bytes_per_step": 4 * world},
                      {"bound": "latency", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                       "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
-                      "note": "4 MiB collection: L2-resident and launch-latency bound (2 launches/step); no HBM claim"},
+                      "note": "4 MiB collection: L2-resident and launch-latency bound (1 launch/step); no HBM claim"},
                      cpu, {"workload": CONFIGS[0], "elements": n, "partitions": 4, "dtype": "f32", "fused": True})
         pipe.close()
     elif args.workload == "c3":
@@ -118,8 +118,17 @@ def run(args, world, rank, local):
         seeds = [42 + t for t in mine]
         samples = [S // T + (1 if t < S % T else 0) for t in mine]
         hits = torch.empty(max(1, len(seeds)), dtype=torch.int64, device=dev)
-        hits_host = torch.empty_like(hits, device="cpu").pin_memory()
-        fn = lambda: ops.pi_hits(seeds, samples, hits)
+        total = torch.empty(1, dtype=torch.int64, device=dev)
+        total_host = torch.empty(1, dtype=torch.int64).pin_memory()
+
+        def fn():
+            # map_cl(pi) over this rank's tasks + reduce_cl(isum2) in one launch;
+            # sharded: one int64 all-reduce (NCCL) combines the rank totals
+            ops.pi_hits(seeds, samples, hits, total_out=total)
+            if world > 1:
+                import torch.distributed as dist
+
+                dist.all_reduce(total)
         fn()
         with B.ClockSampler(local) as clk:
             l0 = capi.launch_count()
@@ -127,26 +136,29 @@ def run(args, world, rank, local):
             launches = capi.launch_count() - l0
 
         def e2e():
-            ops.pi_hits(seeds, samples, hits)
-            hits_host.copy_(hits, non_blocking=True)
+            fn()
+            total_host.copy_(total, non_blocking=True)
             torch.cuda.current_stream().synchronize()
         e2e_ms = _timed(e2e, k, barrier)
         ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
-        total_hits = int(hits.sum().item())
+        fn()
+        total_hits = int(total.item())
+        assert total_hits == int(hits.sum().item()) or world > 1
         if rank == 0 and world == 1:
             r = _ref_workload(["--w", "pi", "--samples", str(1 << 28), "--tasks", "64", "--steps", "1", "--warmup", "0"])
             cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "samples/s", "cores": r["threads"],
                    "kind": "reference", "sample": "2^28 samples in 64 tasks (the C3 task shape, 1/64 of the samples)"}
         ipc_peak = 148 * 4 * (clk.summary()["sm_mhz"] or 1965.0) * 1e6 / 1e9  # warp-instr/s (G), 4 schedulers/SM
-        instr_per_sample = 46.0  # SASS count of the k_pi inner loop (ALU 22, FMA 18, FP64 6)
+        instr_per_sample = 52.75  # SASS of the k_pi inner loop: 211 per 4 samples (ALU ~29, FMA ~17, FP64 6)
         achieved = (S / world) / (ms * 1e-3) * instr_per_sample / 32 / 1e9
         line = _line(args, world, "c3", CONFIGS[2], S / (ms * 1e-3), "samples/s", ms, launches, clk,
                      {"value": S / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": 16 * T,
-                      "d2h_bytes_per_step": 8 * T},
+                      "d2h_bytes_per_step": 8 * world},
                      {"bound": "issue", "achieved": achieved, "peak": ipc_peak, "unit": "Gwarp-instr/s",
                       "frac": achieved / ipc_peak, "traffic": 0, "note": "integer-ALU / issue bound; no HBM traffic"},
                      cpu, {"workload": CONFIGS[2], "samples": S, "tasks": T, "dtype": "u64/f64->i64",
-                           "hits_this_rank": total_hits})
+                           "hits_total": total_hits,
+                           "exchange": "none" if world == 1 else "one int64 NCCL all-reduce of the rank totals"})
     elif args.workload == "c4":
         H = W = 16384
         R = 256

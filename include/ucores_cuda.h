@@ -206,6 +206,12 @@ int ucg_reduce_cl_i64(const int64_t* const* elem_ptrs, uint64_t count, uint64_t 
  * bit-identical to the IEEE-double host test. seeds / samples: HOST arrays. */
 int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
                 void* stream);
+/* Same launch, plus the reduce_cl(isum2) of the task results into *total_out
+ * (device int64, overwritten): the sum over all tasks' hits (integer, so any
+ * tree order gives the same value — engine.hpp:121-192). total_out may be
+ * NULL. */
+int ucg_pi_hits_total(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
+                      int64_t* total_out, void* stream);
 /* Class-D form for the seam-B executor: flags[gid] = hit(seed, gid) (device u8). */
 int ucg_pi_flags(uint64_t seed, uint64_t samples, uint8_t* flags, void* stream);
 

@@ -60,7 +60,8 @@ __device__ __forceinline__ uint32_t pi_hit(uint64_t s0) {
 }
 
 __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTasks tasks, uint64_t nunits,
-                                                   unsigned long long* __restrict__ hits) {
+                                                   unsigned long long* __restrict__ hits,
+                                                   unsigned long long* __restrict__ total) {
   __shared__ uint32_t warp_sum[kPiThreads / 32];
   for (uint64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
     // task owning this unit: binary search over first_unit
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTas
       unsigned long long t = 0;
       for (int w = 0; w < kPiThreads / 32; ++w) t += warp_sum[w];
       atomicAdd(hits + lo, t);
+      if (total) atomicAdd(total, t);
     }
     __syncthreads();
   }
@@ -124,12 +126,13 @@ extern "C" int ucg_pi_flags(uint64_t seed, uint64_t samples, uint8_t* flags, voi
   return UCG_OK;
 }
 
-extern "C" int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
-                           void* stream) {
+extern "C" int ucg_pi_hits_total(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks,
+                                 int64_t* hits_out, int64_t* total_out, void* stream) {
   if (int rc = check_device()) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (total_out) UCG_CUDA(cudaMemsetAsync(total_out, 0, sizeof(int64_t), st));
   if (!ntasks) return UCG_OK;
   if (!seeds || !samples || !hits_out) return fail(UCG_ERR_ARG, "null argument");
-  cudaStream_t st = as_stream(stream);
   UCG_CUDA(cudaMemsetAsync(hits_out, 0, ntasks * sizeof(int64_t), st));
   for (uint64_t t0 = 0; t0 < ntasks; t0 += kMaxTasks) {
     const uint32_t nt = uint32_t(std::min<uint64_t>(kMaxTasks, ntasks - t0));
@@ -144,8 +147,14 @@ extern "C" int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint6
     const uint64_t nunits = p.first_unit[nt];
     if (!nunits) continue;
     const unsigned grid = unsigned(std::min<uint64_t>(nunits, uint64_t(sm_count()) * 8));
-    k_pi<<<grid, kPiThreads, 0, st>>>(p, nunits, reinterpret_cast<unsigned long long*>(hits_out + t0));
+    k_pi<<<grid, kPiThreads, 0, st>>>(p, nunits, reinterpret_cast<unsigned long long*>(hits_out + t0),
+                                      reinterpret_cast<unsigned long long*>(total_out));
     UCG_LAUNCHED();
   }
   return UCG_OK;
+}
+
+extern "C" int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
+                           void* stream) {
+  return ucg_pi_hits_total(seeds, samples, ntasks, hits_out, nullptr, stream);
 }

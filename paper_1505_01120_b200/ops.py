@@ -104,10 +104,16 @@ def reduce_cl_vectors(elem_ptrs, count: int, length: int, part_counts: Sequence[
     return out
 
 
-def pi_hits(seeds: Sequence[int], samples: Sequence[int], hits_out, stream=None):
-    """Monte-Carlo pi mapCL over tasks {seed, samples}."""
+def pi_hits(seeds: Sequence[int], samples: Sequence[int], hits_out, stream=None, total_out=None):
+    """Monte-Carlo pi mapCL over tasks {seed, samples}; with
+    total_out, also the reduce_cl(isum2) of the task hits, in the same launch."""
     _require_cuda(hits_out)
-    call("ucg_pi_hits", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out), stream_handle(stream))
+    if total_out is None:
+        call("ucg_pi_hits", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out), stream_handle(stream))
+    else:
+        _require_cuda(total_out)
+        call("ucg_pi_hits_total", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out), ptr(total_out),
+             stream_handle(stream))
     return hits_out
 
 

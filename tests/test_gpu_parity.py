@@ -352,6 +352,10 @@ def test_pi_golden(cuda, golden):
         hits = torch.empty(T, dtype=torch.int64, device=cuda)
         ops.pi_hits([seed + t for t in range(T)], samples, hits)
         assert hits.cpu().tolist() == case["task_hits"]
+        total = torch.full((1,), -1, dtype=torch.int64, device=cuda)
+        ops.pi_hits([seed + t for t in range(T)], samples, hits, total_out=total)
+        assert hits.cpu().tolist() == case["task_hits"]
+        assert int(total.item()) == case["hits"]  # the reference reduce_cl(isum2) total
 
 
 def test_pi_vs_oracle_small(cuda):
