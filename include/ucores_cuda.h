@@ -83,6 +83,11 @@ int ucg_host_unregister(void* hptr);
 int ucg_memcpy_h2d(void* dst, const void* src, uint64_t bytes, void* stream);
 int ucg_memcpy_d2h(void* dst, const void* src, uint64_t bytes, void* stream);
 int ucg_memcpy_d2d(void* dst, const void* src, uint64_t bytes, void* stream);
+/* Strided copy (cudaMemcpy2DAsync, direction inferred from the pointers, so
+ * host, device and peer-device addresses all work): `rows` rows of
+ * `width_bytes`, source / destination rows `spitch` / `dpitch` bytes apart. */
+int ucg_memcpy2d(void* dst, uint64_t dpitch, const void* src, uint64_t spitch, uint64_t width_bytes,
+                 uint64_t rows, void* stream);
 int ucg_memset(void* dst, int value, uint64_t bytes, void* stream);
 int ucg_stream_create(void** stream_out);
 int ucg_stream_destroy(void* stream);
@@ -90,6 +95,7 @@ int ucg_stream_synchronize(void* stream);
 int ucg_event_create(void** ev_out);
 int ucg_event_destroy(void* ev);
 int ucg_event_record(void* ev, void* stream);
+int ucg_event_synchronize(void* ev);
 int ucg_stream_wait_event(void* stream, void* ev);
 int ucg_event_elapsed_ms(void* ev_start, void* ev_end, float* ms_out); /* synchronizes on ev_end */
 int ucg_device_synchronize(void);

@@ -30,7 +30,11 @@ enum {
   UCD_ERR_OTHER = -14
 };
 
-enum { UCD_MODE_BATCHED = 0, UCD_MODE_PER_TASK = 1 };
+/* BATCHED: Engine + GpuClusterDriver (seam A, one launch per kernel per GPU
+ * per wave); PER_TASK: Engine + GpuWorkerRuntime/CudaExecutor (seam B);
+ * DEVICE: DeviceEngine (device_dataset.hpp) — the dataset is
+ * uploaded once and the chain stays in HBM. */
+enum { UCD_MODE_BATCHED = 0, UCD_MODE_PER_TASK = 1, UCD_MODE_DEVICE = 2 };
 
 const char* ucd_last_error(void);
 

@@ -47,6 +47,7 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_memcpy_h2d": (i32, [vp, vp, u64, vp]),
     "ucg_memcpy_d2h": (i32, [vp, vp, u64, vp]),
     "ucg_memcpy_d2d": (i32, [vp, vp, u64, vp]),
+    "ucg_memcpy2d": (i32, [vp, u64, vp, u64, u64, u64, vp]),
     "ucg_memset": (i32, [vp, C.c_int, u64, vp]),
     "ucg_stream_create": (i32, [P(vp)]),
     "ucg_stream_destroy": (i32, [vp]),
@@ -54,6 +55,7 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_event_create": (i32, [P(vp)]),
     "ucg_event_destroy": (i32, [vp]),
     "ucg_event_record": (i32, [vp, vp]),
+    "ucg_event_synchronize": (i32, [vp]),
     "ucg_stream_wait_event": (i32, [vp, vp]),
     "ucg_event_elapsed_ms": (i32, [vp, vp, P(f32)]),
     "ucg_device_synchronize": (i32, []),

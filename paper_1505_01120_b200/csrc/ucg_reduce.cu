@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "ucg_common.cuh"
@@ -644,6 +645,12 @@ inline bool separate_finish() {
 template <class Op>
 int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float b, float* scratch, float* out,
                    float* result, ucg_xchg* xg, cudaStream_t st) {
+  int dev = -1;
+  UCG_CUDA(cudaGetDevice(&dev));
+  if (dev != t->device) {
+    return fail(UCG_ERR_ARG, "segment table was created on device " + std::to_string(t->device) +
+                                 ", current device is " + std::to_string(dev));
+  }
   FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr, 0};
   if (xg) {
     f.world = xg->world;

@@ -181,6 +181,13 @@ int ucg_memcpy_d2d(void* dst, const void* src, uint64_t bytes, void* stream) {
   UCG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
   return UCG_OK;
 }
+int ucg_memcpy2d(void* dst, uint64_t dpitch, const void* src, uint64_t spitch, uint64_t width_bytes,
+                 uint64_t rows, void* stream) {
+  if (!width_bytes || !rows) return UCG_OK;
+  if (!dst || !src) return fail(UCG_ERR_ARG, "null pointer");
+  UCG_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, rows, cudaMemcpyDefault, as_stream(stream)));
+  return UCG_OK;
+}
 int ucg_memset(void* dst, int value, uint64_t bytes, void* stream) {
   if (!bytes) return UCG_OK;
   UCG_CUDA(cudaMemsetAsync(dst, value, bytes, as_stream(stream)));
@@ -214,6 +221,10 @@ int ucg_event_destroy(void* ev) {
 }
 int ucg_event_record(void* ev, void* stream) {
   UCG_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), as_stream(stream)));
+  return UCG_OK;
+}
+int ucg_event_synchronize(void* ev) {
+  UCG_CUDA(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(ev)));
   return UCG_OK;
 }
 int ucg_stream_wait_event(void* stream, void* ev) {
@@ -315,11 +326,15 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
 
 int ucg_segtab_destroy(ucg_segtab* t) {
   if (!t) return UCG_OK;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != t->device) cudaSetDevice(t->device);  // free on the table's own device
   cudaFree(t->d_begin);
   cudaFree(t->d_len);
   cudaFree(t->d_first_item);
   cudaFree(t->d_item_seg);
   cudaFree(t->d_done);
+  if (cur >= 0 && cur != t->device) cudaSetDevice(cur);
   delete t;
   return UCG_OK;
 }

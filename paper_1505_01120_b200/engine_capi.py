@@ -12,7 +12,7 @@ from . import capi
 from .errors import ArityMismatch, EmptyDataset, Error, JobFailed, UnknownKernel
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libucores_engine.so"
-MODE = {"batched": 0, "per_task": 1}
+MODE = {"batched": 0, "per_task": 1, "device": 2}
 _lib = None
 
 

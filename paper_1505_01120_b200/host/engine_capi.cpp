@@ -9,6 +9,7 @@
 #include "ucores/dataset.hpp"
 #include "ucores/engine.hpp"
 #include "ucores/errors.hpp"
+#include "ucores_b200/device_dataset.hpp"
 #include "ucores_b200/device_ops.hpp"
 #include "ucores_b200/gpu_cluster_driver.hpp"
 #include "ucores_b200/kernels.hpp"
@@ -58,12 +59,43 @@ int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts,
     p.a = a;
     p.b = b;
     register_workload(reg, ops, p);
+    const std::string pk = op == 1 ? "pmax" : "psum", rk = op == 1 ? "max2" : "sum2";
+    if (mode == UCD_MODE_DEVICE) {
+      // the device-resident engine: one upload, the chain in HBM, one element back
+      DeviceEngine de(p, gpus);
+      auto t0 = std::chrono::steady_clock::now();
+      std::vector<Partition> parts(nparts);
+      std::uint64_t off = 0;
+      for (std::uint64_t q = 0; q < nparts; ++q) {
+        parts[q].elements.push_back(Element::f32(std::vector<float>(x + off, x + off + part_lens[q])));
+        off += part_lens[q];
+      }
+      Dataset d(std::move(parts));
+      DeviceDataset y = de.map_cl(de.upload(d), "axpb");
+      DeviceDataset ps = de.map_cl_partition(y, pk);
+      Element r = de.reduce_cl(ps, rk);
+      auto t1 = std::chrono::steady_clock::now();
+      if (seconds_out) *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+      if (result_out) *result_out = r.as_f32()[0];
+      if (y_out) {
+        std::uint64_t o = 0;
+        for (const Element& e : de.collect(y).collect()) {
+          auto v = e.as_f32();
+          std::memcpy(y_out + o, v.data(), v.size_bytes());
+          o += v.size();
+        }
+      }
+      if (partials_out) {
+        std::uint64_t q = 0;
+        for (const Element& e : de.collect(ps).collect()) partials_out[q++] = e.as_f32()[0];
+      }
+      return;
+    }
     GpuClusterDriver::Options opt;
     opt.max_gpus = gpus;
     opt.mode = mode == UCD_MODE_PER_TASK ? GpuClusterDriver::Mode::PerTask : GpuClusterDriver::Mode::Batched;
     GpuClusterDriver drv(reg, ops, opt);
     Engine eng(drv, reg);
-    const std::string pk = op == 1 ? "pmax" : "psum", rk = op == 1 ? "max2" : "sum2";
 
     auto t0 = std::chrono::steady_clock::now();
     std::vector<Partition> parts(nparts);

@@ -19,6 +19,7 @@
 #include "ucores/engine.hpp"
 #include "ucores/worker.hpp"
 #include "ucores_b200/cuda_executor.hpp"
+#include "ucores_b200/device_dataset.hpp"
 #include "ucores_b200/device_ops.hpp"
 #include "ucores_b200/gpu_cluster_driver.hpp"
 #include "ucores_b200/kernels.hpp"
@@ -355,6 +356,159 @@ int main() {
     EXPECT(same(yh, yg), "y bitwise");
     EXPECT(rg == rh, "sum bitwise");
     std::printf("  engine e2e: gpu %.1f ms, host-seq %.1f ms\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
+  });
+
+  // ---- DeviceEngine: device-resident chains vs the reference Engine ----
+  WorkloadParams dparams;
+  dparams.sobel_width = 48;
+  dparams.matmul_n = 256;
+  DeviceEngine de(dparams);
+
+  run_case("device dataset: upload/collect round trip, all array kinds", [&] {
+    std::vector<Partition> parts(4);
+    parts[0].elements = {Element::f32({1.5f, -0.0f, 3e38f}), Element::f32({})};
+    parts[2].elements = {Element::i64({-1, 1ll << 62}), Element::i64({7})};
+    parts[3].elements = {Element::bytes("hello"), Element::bytes(std::string(1000, 'x'))};
+    Dataset d(std::move(parts));
+    EXPECT(same(d, de.collect(de.upload(d))), "collect(upload(d)) == d");
+  });
+
+  run_case("device dataset: C1 chains bitwise vs host Engine (packed and ragged elements)", [&] {
+    for (auto [n, elems, parts] : std::vector<std::tuple<std::size_t, std::size_t, std::size_t>>{
+             {1u << 20, 4, 4}, {100003, 13, 5}, {70001, 7, 3}, {4099, 33, 6}}) {
+      std::vector<std::vector<float>> es(elems);
+      std::size_t pos = 0;
+      for (std::size_t k = 0; k < elems; ++k) {
+        es[k].resize(n / elems + (k < n % elems ? 1 : 0));
+        for (auto& v : es[k]) v = u01(777, pos++);
+      }
+      Dataset x = f32_dataset(es, parts);
+      DeviceDataset dx = de.upload(x);
+      Dataset yh = eh.map_cl(x, "axpb");
+      DeviceDataset dy = de.map_cl(dx, "axpb");
+      EXPECT(same(yh, de.collect(dy)), "device map_cl(axpb) bitwise");
+      for (const char* op : {"sum", "max"}) {
+        const std::string pk = std::string("p") + op, rk = std::string(op) + "2";
+        Dataset ph = eh.map_cl_partition(yh, pk);
+        DeviceDataset dp = de.map_cl_partition(dy, pk);
+        EXPECT(same(ph, de.collect(dp)), "device map_cl_partition bitwise");
+        EXPECT(eh.reduce_cl(ph, rk) == de.reduce_cl(dp, rk), "device reduce_cl bitwise");
+        // per-element psum (map_cl) and reduce_cl straight over the mapped vectors' partials
+        Dataset eph = eh.map_cl(yh, pk);
+        DeviceDataset edp = de.map_cl(dy, pk);
+        EXPECT(same(eph, de.collect(edp)), "device map_cl(psum) per element bitwise");
+        EXPECT(eh.reduce_cl(eph, rk) == de.reduce_cl(edp, rk), "device reduce_cl over element partials");
+      }
+    }
+  });
+
+  run_case("device dataset: reduce_cl vectoradd / isum2 with empty and ragged partitions", [&] {
+    std::uint64_t s = 11;
+    for (int c = 0; c < 12; ++c) {
+      const std::size_t count = 1 + kernels::mix64(s++) % 30, parts = 1 + kernels::mix64(s++) % 12,
+                        len = 1 + kernels::mix64(s++) % 300;
+      std::vector<Element> ef, ei;
+      for (std::size_t i = 0; i < count; ++i) {
+        std::vector<float> vf(len);
+        std::vector<std::int64_t> vi(len);
+        for (std::size_t j = 0; j < len; ++j) {
+          vf[j] = 2.0f * u01(s, j) - 1.0f;
+          vi[j] = static_cast<std::int64_t>(kernels::mix64(s + j));
+        }
+        ++s;
+        ef.push_back(Element::f32(vf));
+        ei.push_back(Element::i64(vi));
+      }
+      Dataset df = create_dataset(std::move(ef), parts), di = create_dataset(std::move(ei), parts);
+      EXPECT(eh.reduce_cl(df, "vectoradd") == de.reduce_cl(de.upload(df), "vectoradd"), "vectoradd bitwise");
+      EXPECT(eh.reduce_cl(df, "max2") == de.reduce_cl(de.upload(df), "max2"), "max2 bitwise");
+      EXPECT(eh.reduce_cl(di, "isum2") == de.reduce_cl(de.upload(di), "isum2"), "isum2 exact");
+    }
+  });
+
+  run_case("device dataset: pi map_cl + isum2, sobel, matmul", [&] {
+    std::vector<Element> es;
+    for (int t = 0; t < 8; ++t) es.push_back(Element::i64({42 + t, 500000}));
+    Dataset d = create_dataset(std::move(es), 3);
+    DeviceDataset hits = de.map_cl(de.upload(d), "pi");
+    EXPECT(same(eh.map_cl(d, "pi"), de.collect(hits)), "pi {hits, samples} bitwise");
+    EXPECT(de.reduce_cl(hits, "isum2").as_i64()[0] == 3141371, "pi total 3141371");
+
+    const std::size_t H = 50, W = 48, R = 16;
+    std::vector<Element> bands;
+    for (std::size_t r0 = 0; r0 < H; r0 += R) {
+      const std::size_t rr = std::min(R, H - r0);
+      std::vector<std::uint8_t> b((rr + 2) * W);
+      for (std::size_t i = 0; i < b.size(); ++i)
+        b[i] = static_cast<std::uint8_t>(kernels::mix64(9 + r0 * W + i) >> 56);
+      bands.push_back(Element::bytes(b));
+    }
+    Dataset sb = create_dataset(std::move(bands), 2);
+    EXPECT(same(eh.map_cl(sb, "sobel"), de.collect(de.map_cl(de.upload(sb), "sobel"))), "sobel per band bitwise");
+    Dataset one = create_dataset(std::vector<Element>(sb.partitions()[0].elements.begin(),
+                                                      sb.partitions()[0].elements.begin() + 1), 1);
+    EXPECT(same(eh.map_cl_partition(one, "sobel"), de.collect(de.map_cl_partition(de.upload(one), "sobel"))),
+           "sobel map_cl_partition bitwise");
+
+    const std::size_t n = 256;
+    std::vector<std::vector<float>> ab(2, std::vector<float>(2 * n * n));
+    for (std::size_t e = 0; e < 2; ++e)
+      for (std::size_t i = 0; i < 2 * n * n; ++i) ab[e][i] = 2.0f * u01(200 + e, i) - 1.0f;
+    Dataset md = f32_dataset(ab, 1);  // two elements in one partition: per-element GEMMs
+    Dataset h = eh.map_cl(md, "matmul"), g = de.collect(de.map_cl(de.upload(md), "matmul"));
+    for (std::size_t e = 0; e < 2; ++e) {
+      auto a = h.partitions()[0].elements[e].as_f32();
+      auto b = g.partitions()[0].elements[e].as_f32();
+      double ss = 0, md2 = 0;
+      for (std::size_t i = 0; i < a.size(); ++i) {
+        ss += double(a[i]) * a[i];
+        md2 = std::max(md2, std::abs(double(a[i]) - b[i]));
+      }
+      EXPECT(md2 <= 1e-2 * std::sqrt(ss / a.size()), "device matmul within TF32 tolerance");
+    }
+  });
+
+  run_case("device dataset: errors as the reference Engine", [&] {
+    auto throws = [](auto fn, auto tag) {
+      try {
+        fn();
+      } catch (const decltype(tag)&) {
+        return true;
+      } catch (...) {
+        return false;
+      }
+      return false;
+    };
+    DeviceDataset holes = de.upload(f32_dataset({{1.0f}, {2.0f}}, 3));
+    EXPECT(throws([&] { de.map_cl_partition(holes, "psum"); }, JobFailed("")), "empty partition -> JobFailed");
+    EXPECT(throws([&] { de.reduce_cl(de.upload(Dataset(std::vector<Partition>(2))), "sum2"); }, EmptyDataset("")),
+           "EmptyDataset");
+    EXPECT(throws([&] { de.reduce_cl(de.upload(f32_dataset({{1.0f, 2.0f}, {1.0f}}, 1)), "sum2"); }, JobFailed("")),
+           "length mismatch -> JobFailed");
+    EXPECT(throws([&] { de.map_cl(holes, "nosuch"); }, UnknownKernel("")), "UnknownKernel");
+    EXPECT(throws([&] { de.map_cl(de.upload(create_dataset({Element::bytes("ab")}, 1)), "axpb"); }, JobFailed("")),
+           "kind mismatch -> JobFailed");
+    Element r = de.reduce_cl(de.upload(f32_dataset({{3.5f, 4.5f}}, 4)), "sum2");
+    EXPECT(r.as_f32().size() == 2 && r.as_f32()[0] == 3.5f, "single element returned as is");
+  });
+
+  run_case("device dataset: C2-shaped chain at 2^27, one upload, one result back", [&] {
+    const std::size_t P = 16, L = 1u << 23;
+    std::vector<std::vector<float>> es(P, std::vector<float>(L));
+    for (std::size_t p = 0; p < P; ++p)
+      for (std::size_t i = 0; i < L; ++i) es[p][i] = u01(1000 + p, i);
+    Dataset x = f32_dataset(es, P);
+    es.clear();
+    auto t0 = std::chrono::steady_clock::now();
+    DeviceDataset dx = de.upload(x);
+    auto t1 = std::chrono::steady_clock::now();
+    Element rd = de.reduce_cl(de.map_cl_partition(de.map_cl(dx, "axpb"), "psum"), "sum2");
+    auto t2 = std::chrono::steady_clock::now();
+    Element rh = eh.reduce_cl(eh.map_cl_partition(eh.map_cl(x, "axpb"), "psum"), "sum2");
+    EXPECT(rd == rh, "sum bitwise vs host Engine");
+    std::printf("  device engine: upload %.1f ms, chain %.2f ms\n",
                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
                 std::chrono::duration<double, std::milli>(t2 - t1).count());
   });

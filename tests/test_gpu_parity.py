@@ -398,7 +398,7 @@ def test_sobel_golden_and_random(cuda, golden):
 
 # ---- the reference Engine through the C++ drop-in (libucores_engine.so) ------------
 
-@pytest.mark.parametrize("mode", ["batched", "per_task"])
+@pytest.mark.parametrize("mode", ["batched", "per_task", "device"])
 def test_engine_capi_pipeline(cuda, golden, mode):
     from paper_1505_01120_b200 import engine_capi
 
