@@ -208,12 +208,10 @@ class DeviceEngine {
     }
     DeviceDataset out = allocate(std::move(parts));
     for (std::size_t p = 0; p < out.parts_.size(); ++p) {
-      std::uint8_t* dst = out.data(p);
-      for (const ucores::Element& e : d.partitions()[p].elements) {
-        const std::uint64_t n = e.byte_size();
-        upload_bytes(out.parts_[p].gpu, dst, static_cast<const std::uint8_t*>(host_bytes(e)), n);
-        dst += n;
-      }
+      std::vector<std::pair<const std::uint8_t*, std::uint64_t>> pieces;
+      for (const ucores::Element& e : d.partitions()[p].elements)
+        pieces.emplace_back(static_cast<const std::uint8_t*>(host_bytes(e)), e.byte_size());
+      upload_partition(out.parts_[p].gpu, out.data(p), pieces);
     }
     sync_all();
     return out;
@@ -556,12 +554,19 @@ class DeviceEngine {
     int next = 0;
   };
 
-  void upload_bytes(std::size_t g, std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n) {
+  // A partition's element payloads, packed back to back (its device layout)
+  // through the staging halves: one DMA per filled half, so a partition of
+  // 2^18 one-float elements is one copy, not 2^18.
+  void upload_partition(std::size_t g, std::uint8_t* dst,
+                        const std::vector<std::pair<const std::uint8_t*, std::uint64_t>>& pieces) {
     Gpu& gpu = *gpus_[g];
     DeviceGuard guard;
     gpu.bind();
-    if (n < kDirectBytes) {
-      check(ucg_memcpy_h2d(dst, src, n, gpu.stream()));
+    std::uint64_t total = 0;
+    for (const auto& pc : pieces) total += pc.second;
+    if (total == 0) return;
+    if (pieces.size() == 1 && total < kDirectBytes) {
+      check(ucg_memcpy_h2d(dst, pieces[0].first, total, gpu.stream()));
       return;
     }
     if (staging_.size() < gpus_.size()) staging_.resize(gpus_.size());
@@ -573,24 +578,47 @@ class DeviceEngine {
       }
     }
     const unsigned threads = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-    for (std::uint64_t off = 0; off < n; off += kStageBytes) {
-      const std::uint64_t len = std::min(kStageBytes, n - off);
-      const int k = s.next;
+    std::uint8_t* stage = nullptr;
+    std::uint64_t fill = 0, dev_off = 0;
+    int k = 0;
+    auto acquire = [&] {
+      k = s.next;
       s.next ^= 1;
-      if (s.busy[k]) check(ucg_event_synchronize(s.ev[k]));  // that half's previous copy is done
-      auto* stage = static_cast<std::uint8_t*>(s.buf[k]);
-      const std::uint64_t per = (len + threads - 1) / threads;
-      std::vector<std::thread> pool;
-      for (unsigned t = 1; t < threads; ++t) {
-        const std::uint64_t b = std::min(len, t * per), e = std::min(len, b + per);
-        if (b < e) pool.emplace_back([=] { std::memcpy(stage + b, src + off + b, e - b); });
-      }
-      std::memcpy(stage, src + off, std::min(len, per));
-      for (auto& th : pool) th.join();
-      check(ucg_memcpy_h2d(dst + off, stage, len, gpu.stream()));
+      if (s.busy[k]) check(ucg_event_synchronize(s.ev[k]));  // that half's previous DMA is done
+      stage = static_cast<std::uint8_t*>(s.buf[k]);
+      fill = 0;
+    };
+    auto flush = [&] {
+      if (!fill) return;
+      check(ucg_memcpy_h2d(dst + dev_off, stage, fill, gpu.stream()));
       check(ucg_event_record(s.ev[k], gpu.stream()));
       s.busy[k] = true;
+      dev_off += fill;
+      fill = 0;
+      stage = nullptr;
+    };
+    for (const auto& [src, n] : pieces) {
+      for (std::uint64_t off = 0; off < n;) {
+        if (!stage) acquire();
+        const std::uint64_t len = std::min(kStageBytes - fill, n - off);
+        if (len >= (1u << 20) && threads > 1) {  // large piece: parallel host copy
+          const std::uint64_t per = (len + threads - 1) / threads;
+          std::vector<std::thread> pool;
+          for (unsigned t = 1; t < threads; ++t) {
+            const std::uint64_t b = std::min(len, t * per), e = std::min(len, b + per);
+            if (b < e) pool.emplace_back([=] { std::memcpy(stage + fill + b, src + off + b, e - b); });
+          }
+          std::memcpy(stage + fill, src + off, std::min(len, per));
+          for (auto& th : pool) th.join();
+        } else {
+          std::memcpy(stage + fill, src + off, len);
+        }
+        fill += len;
+        off += len;
+        if (fill == kStageBytes) flush();
+      }
     }
+    flush();
   }
 
   // -- helpers ----------------------------------------------------------------------

@@ -494,6 +494,26 @@ int main() {
     EXPECT(r.as_f32().size() == 2 && r.as_f32()[0] == 3.5f, "single element returned as is");
   });
 
+  run_case("device dataset: C1 literal form (one float per element)", [&] {
+    for (std::size_t n : {std::size_t(1) << 16, std::size_t(1) << 20}) {
+      std::vector<Element> es;
+      es.reserve(n);
+      for (std::size_t i = 0; i < n; ++i) es.push_back(Element::f32({u01(12345, i)}));
+      Dataset x = create_dataset(std::move(es), 4);
+      auto t0 = std::chrono::steady_clock::now();
+      DeviceDataset dy = de.map_cl(de.upload(x), "axpb");
+      Element rd = de.reduce_cl(de.map_cl_partition(dy, "psum"), "sum2");
+      auto t1 = std::chrono::steady_clock::now();
+      if (n <= (1u << 16)) {  // the host Engine runs one task per element: keep it small
+        Dataset yh = eh.map_cl(x, "axpb");
+        EXPECT(same(yh, de.collect(dy)), "literal map_cl bitwise");
+        EXPECT(eh.reduce_cl(eh.map_cl_partition(yh, "psum"), "sum2") == rd, "literal chain bitwise");
+      }
+      std::printf("  literal 2^%d elements: device chain incl. upload %.2f ms\n", int(std::log2(double(n))),
+                  std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
+  });
+
   run_case("device dataset: C2-shaped chain at 2^27, one upload, one result back", [&] {
     const std::size_t P = 16, L = 1u << 23;
     std::vector<std::vector<float>> es(P, std::vector<float>(L));
@@ -501,6 +521,7 @@ int main() {
       for (std::size_t i = 0; i < L; ++i) es[p][i] = u01(1000 + p, i);
     Dataset x = f32_dataset(es, P);
     es.clear();
+    de.upload(x);  // first use: pinned staging and pool allocations
     auto t0 = std::chrono::steady_clock::now();
     DeviceDataset dx = de.upload(x);
     auto t1 = std::chrono::steady_clock::now();
