@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-engine-e2e", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "wc"],
                     help="c2 (default) is the headline; the others are the remaining BASELINE configs")
     ap.add_argument("--cpu-sample-parts", type=int, default=4)
     return ap.parse_args()

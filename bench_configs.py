@@ -6,6 +6,7 @@ bench.py (imported by `bench.py --workload c1|c3|c4|c5`):
   c3  Monte-Carlo pi via mapCL, 2^34 samples in 64 tasks (exact counts)
   c4  mapCLPartition 3x3 Sobel on a 16384x16384 u8 image in 64 row bands
   c5  mapCL dense fp32 matmul 8192^3 per partition, 8 partitions, tcgen05
+  wc  WordCount word-start flags over 1 GiB of text in 64 chunks (§8(f)4)
 
 Units (tasks / bands / partitions) are split over the ranks in contiguous
 blocks; value = all units / max-over-ranks device time. The reference CPU
@@ -244,6 +245,61 @@ def run(args, world, rank, local):
                      {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s", "frac": per_gpu / peak,
                       "traffic": None, "peak_kind": "cuBLAS TF32 8192^3 measured in this run"},
                      cpu, {"workload": CONFIGS[4], "n": n, "partitions": P, "dtype": "tf32 (fp32 in/out, fp32 accumulate)"})
+    elif args.workload == "wc":
+        # WordCount word-start flags over create_from_text chunks.
+        # Every chunk ends on a delimiter (dataset.hpp:94-112), so the flags of
+        # the concatenated chunks are the concatenation of per-chunk flags: one
+        # launch covers all of a GPU's chunks.
+        total, chunks = 1 << 30, 64
+        per = total // chunks
+        mine = shard_range(chunks, world, rank)
+        ln = len(mine)
+        text = torch.empty(max(1, ln) * per, dtype=torch.uint8, device=dev)
+        ops.fill_bytes_(text, 11)
+        alphabet = (b" \t\n\r" * 12 + b"abcdefghijklmnopqrstuvwxyz0123456789" * 6)[:256]
+        lut = torch.tensor(list(alphabet.ljust(256, b"e")), dtype=torch.uint8, device=dev)
+        step_b = 1 << 26
+        for o in range(0, text.numel(), step_b):
+            seg = text[o:o + step_b]
+            seg.copy_(lut[seg.to(torch.int32)])
+        text.view(max(1, ln), per)[:, -1] = ord("\n")  # chunk ends on a delimiter
+        flags = torch.empty_like(text)
+        fn = lambda: ops.word_start_flags(text, flags)
+        fn()
+        with B.ClockSampler(local) as clk:
+            l0 = capi.launch_count()
+            ms = _timed(fn, k, barrier)
+            launches = capi.launch_count() - l0
+        host_in = torch.empty_like(text, device="cpu").pin_memory()
+        host_in.copy_(text)
+        host_out = torch.empty_like(flags, device="cpu").pin_memory()
+
+        def e2e():
+            text.copy_(host_in, non_blocking=True)
+            fn()
+            host_out.copy_(flags, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_ms = _timed(e2e, k, barrier)
+        ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
+        words = int(flags.sum(dtype=torch.int64).item()) if ln else 0
+        if rank == 0 and world == 1:
+            r = _ref_workload(["--w", "wordcount", "--bytes", str(1 << 26), "--chunk", str(1 << 22), "--steps", "1",
+                               "--warmup", "0"])
+            cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "bytes/s", "cores": r["threads"],
+                   "kind": "reference",
+                   "sample": ("64 MiB synthetic corpus in 4 MiB create_from_text chunks, map_cl(wordcount): per-byte "
+                              "word-start flags (run) + tokenised tables (map_return_value, host)")}
+        algo = 2 * ln * per
+        achieved = algo / (ms * 1e-3) / 1e9
+        line = _line(args, world, "wc", "WordCount word-start flags over create_from_text chunks (SURVEY 8(f)4)",
+                     total / (ms * 1e-3), "bytes/s", ms, launches, clk,
+                     {"value": total / (e2e_ms * 1e-3), "unit": "bytes/s", "h2d_bytes_per_step": total,
+                      "d2h_bytes_per_step": total, "note": "text up, flags down (the host tokeniser's input)"},
+                     {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                      "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
+                      "algorithmic_bytes_per_launch": algo},
+                     cpu, {"workload": "1 GiB synthetic text in 64 chunks of 16 MiB, word-start flags (u8 per byte)",
+                           "bytes": total, "chunks": chunks, "dtype": "u8", "word_starts_this_rank": words})
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -768,9 +768,11 @@ json run_golden() {
 //   --w pi      --samples S --tasks T          (C3 shape, S scaled down)
 //   --w sobel   --height H --width W --rows R  (C4: bands of R rows, halos)
 //   --w matmul  --n N --parts P                (C5 shape at a small n)
+//   --w wordcount --bytes B --chunk C          (create_from_text chunks -> map_cl(wordcount))
 int run_bench_workload(int argc, char** argv) {
   std::string w = "pi";
   std::uint64_t samples = 1u << 26, tasks = 64, H = 2048, W = 16384, R = 256, n = 256, parts = 2;
+  std::uint64_t bytes = 64ull << 20, chunk = 1ull << 20;
   unsigned threads = std::thread::hardware_concurrency();
   int steps = 2, warmup = 1;
   for (int i = 2; i + 1 < argc; i += 2) {
@@ -783,6 +785,8 @@ int run_bench_workload(int argc, char** argv) {
     else if (k == "--rows") R = std::stoull(v);
     else if (k == "--n") n = std::stoull(v);
     else if (k == "--parts") parts = std::stoull(v);
+    else if (k == "--bytes") bytes = std::stoull(v);
+    else if (k == "--chunk") chunk = std::stoull(v);
     else if (k == "--threads") threads = static_cast<unsigned>(std::stoul(v));
     else if (k == "--steps") steps = std::stoi(v);
     else if (k == "--warmup") warmup = std::stoi(v);
@@ -819,6 +823,21 @@ int run_bench_workload(int argc, char** argv) {
     d = f32_dataset(es, parts);
     kernel = "matmul";
     units = 2.0 * double(n) * double(n) * double(n) * double(parts);
+  } else if (w == "wordcount") {
+    // the reference chunker (dataset.hpp:94-112) over a synthetic corpus file;
+    // "wordcount" prefers device execution, so the host executor runs the
+    // per-byte run() (word-start flags) and map_return_value tokenises
+    std::string corpus;
+    for (std::uint64_t seed = 5; corpus.size() < bytes; ++seed) corpus += make_corpus(seed * 1000003, 100000);
+    corpus.resize(bytes);
+    const std::string path = "/tmp/ucores_wc_bench.txt";
+    {
+      std::ofstream f(path, std::ios::binary);
+      f << corpus;
+    }
+    d = create_from_text(path, chunk);
+    kernel = "wordcount";
+    units = double(bytes);
   } else {
     throw Error("unknown workload " + w);
   }

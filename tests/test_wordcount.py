@@ -58,3 +58,30 @@ def test_word_flags_gpu_bitexact(cuda, case):
         ops.word_start_flags(buf[off:off + len(data)], flags[off:off + len(data)])
         got = flags[off:off + len(data)].cpu().numpy()
         assert np.array_equal(got, want)
+
+
+def test_chunk_flags_concatenate():
+    """create_from_text cuts after a delimiter (dataset.hpp:94-112), so the
+    flags of the whole text equal the per-chunk flags concatenated: one launch
+    can cover every chunk of a GPU (bench.py --workload wc)."""
+    data = O.corpus(9, 20000)
+    chunks = O.chunk_offsets(data, 4096)
+    assert len(chunks) > 10
+    whole = O.word_start_flags(data)
+    per = np.concatenate([O.word_start_flags(data[b:e]) for b, e in chunks])
+    assert np.array_equal(whole, per)
+
+
+@pytest.mark.gpu
+def test_word_flags_gpu_whole_text_equals_chunks(cuda):
+    import torch
+
+    from paper_1505_01120_b200 import ops
+
+    data = O.corpus(13, 200000)
+    chunks = O.chunk_offsets(data, 65536)
+    buf = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(cuda)
+    flags = torch.empty_like(buf)
+    ops.word_start_flags(buf, flags)
+    want = np.concatenate([O.word_start_flags(data[b:e]) for b, e in chunks])
+    assert np.array_equal(flags.cpu().numpy(), want)
