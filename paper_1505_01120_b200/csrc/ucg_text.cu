@@ -2,12 +2,13 @@
 //
 // flags[gid] = 1 iff byte[gid] is a word character and (gid == 0 or
 // byte[gid-1] is a delimiter); delimiters are ASCII space, tab, LF, CR
-// (ucores/dataset.hpp:87-89). One thread owns 16 bytes (one 128-bit load and
-// store), the byte before its span comes from the previous thread by shuffle
-// (lane 0 loads it). 2 B/byte of HBM traffic.
+// (ucores/dataset.hpp:87-89). Lanes own 16-byte words (128-bit loads and
+// stores, 4 in flight per lane); the byte before a word comes from the
+// neighbouring lane by shuffle. 2 B/byte of HBM traffic.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ucg_common.cuh"
 
@@ -21,23 +22,70 @@ __device__ __forceinline__ uint32_t delim_mask(uint32_t w) {
   return (sp | tb | lf | cr) & 0x01010101u;
 }
 
+// flags of one 16-byte word given its delimiter masks and the delimiter flag
+// (0/1) of the byte before it
+__device__ __forceinline__ uint4 word_flags16(const uint4& w, uint32_t prev_delim) {
+  const uint32_t d[4] = {delim_mask(w.x), delim_mask(w.y), delim_mask(w.z), delim_mask(w.w)};
+  uint32_t f[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    // delimiter flags of the byte before each byte of word k
+    const uint32_t before = (d[k] << 8) | (k ? d[k - 1] >> 24 : prev_delim);
+    f[k] = (d[k] ^ 0x01010101u) & before;  // word char preceded by a delimiter
+  }
+  return make_uint4(f[0], f[1], f[2], f[3]);
+}
+
+// A warp walks blocks of kWU x 512 contiguous bytes (grid-stride) and loads
+// the next block while it finishes the current one: lane l holds the 16-byte
+// words (u*32 + l), u < kWU. The byte before lane
+// l's word is the last byte of lane l-1's word (shuffle); lane 0 takes it
+// from lane 31 of the previous row, and a block's first byte looks back with
+// one scalar load.
+template <int kWU>
 __global__ void __launch_bounds__(256) k_word_flags(const uint8_t* __restrict__ in, uint8_t* __restrict__ flags,
                                                     uint64_t n16) {
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
-    const uint4 w = __ldcs(reinterpret_cast<const uint4*>(in) + i);
-    // previous byte: 1 = "before the chunk" counts as a delimiter (gid == 0 rule)
-    uint32_t prev_delim = 1;
-    if (i > 0) prev_delim = delim_mask(in[16 * i - 1]) & 1u;
-    const uint32_t d[4] = {delim_mask(w.x), delim_mask(w.y), delim_mask(w.z), delim_mask(w.w)};
-    uint32_t f[4];
+  const int lane = threadIdx.x & 31;
+  const uint64_t nblk = n16 / (32 * kWU);
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint4* src = reinterpret_cast<const uint4*>(in);
+  uint4* dst = reinterpret_cast<uint4*>(flags);
+  uint64_t b = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  uint4 w[kWU];
+  if (b < nblk) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      // delimiter flags of the byte before each byte of word k
-      const uint32_t before = (d[k] << 8) | (k ? d[k - 1] >> 24 : prev_delim);
-      f[k] = (d[k] ^ 0x01010101u) & before;  // word char preceded by a delimiter
+    for (int u = 0; u < kWU; ++u) w[u] = __ldcs(src + b * 32 * kWU + u * 32 + lane);
+  }
+  while (b < nblk) {
+    const uint64_t nb = b + nwarps;
+    uint4 nx[kWU];
+    if (nb < nblk) {
+#pragma unroll
+      for (int u = 0; u < kWU; ++u) nx[u] = __ldcs(src + nb * 32 * kWU + u * 32 + lane);
     }
-    __stcs(reinterpret_cast<uint4*>(flags) + i, make_uint4(f[0], f[1], f[2], f[3]));
+    const uint64_t w0 = b * 32 * kWU;
+    // previous byte's delimiter flag; "before the text" counts as a delimiter
+    uint32_t carry = 1;
+    if (lane == 0 && w0 > 0) carry = delim_mask(in[16 * w0 - 1]) & 1u;
+#pragma unroll
+    for (int u = 0; u < kWU; ++u) {
+      const uint32_t last = delim_mask(w[u].w) >> 24;  // this lane's last byte
+      const uint32_t up = __shfl_up_sync(0xffffffffu, last, 1);
+      const uint32_t prev = lane ? up : carry;
+      carry = __shfl_sync(0xffffffffu, last, 31);     // for lane 0 of the next row
+      __stcs(dst + w0 + u * 32 + lane, word_flags16(w[u], prev));
+    }
+#pragma unroll
+    for (int u = 0; u < kWU; ++u) w[u] = nx[u];
+    b = nb;
+  }
+  // words past the last full block: one per thread
+  const uint64_t tail0 = nblk * 32 * kWU;
+  for (uint64_t i = tail0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint4 v = __ldcs(src + i);
+    const uint32_t prev = i > 0 ? (delim_mask(in[16 * i - 1]) & 1u) : 1u;
+    __stcs(dst + i, word_flags16(v, prev));
   }
 }
 
@@ -62,8 +110,17 @@ extern "C" int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* f
   uint64_t done = 0;
   if (aligned16(bytes) && aligned16(flags) && n >= 16) {
     const uint64_t n16 = n / 16;
-    const unsigned grid = unsigned(std::min<uint64_t>((n16 + 255) / 256, uint64_t(sm_count()) * 8));
-    k_word_flags<<<grid, 256, 0, st>>>(bytes, flags, n16);
+    static const int variant = [] {
+      const char* e = getenv("UCG_WC_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+    const int wu = variant == 1 ? 8 : variant == 3 ? 2 : 4;
+    const int per_sm = variant == 2 ? 4 : variant == 3 ? 16 : 8;
+    const uint64_t warps = std::max<uint64_t>(1, n16 / (32 * wu));
+    const unsigned grid = unsigned(std::min<uint64_t>((warps + 7) / 8, uint64_t(sm_count()) * per_sm));
+    if (wu == 8) k_word_flags<8><<<grid, 256, 0, st>>>(bytes, flags, n16);
+    else if (wu == 2) k_word_flags<2><<<grid, 256, 0, st>>>(bytes, flags, n16);
+    else k_word_flags<4><<<grid, 256, 0, st>>>(bytes, flags, n16);
     UCG_LAUNCHED();
     done = n16 * 16;
   }
