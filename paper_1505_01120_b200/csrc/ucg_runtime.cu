@@ -268,13 +268,19 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if (int rc = check_device()) return rc;
   if (nseg && (!begin || !len)) return fail(UCG_ERR_ARG, "begin/len is null");
   if (nseg >= (1ull << 32)) return fail(UCG_ERR_ARG, "too many segments");
-  // work-item size: 2^12 floats (16 KB; items are claimed dynamically, so
-  // no wave quantisation to fit), 2^11 when that leaves fewer items than
-  // resident warps. Sweep: tools/scaling_probe.py (2^12 best from 2^27 to
-  // 2^30 elements; 2^11 restarts the load pipeline too often).
-  uint64_t items12 = 0;
-  for (uint64_t s = 0; s < nseg; ++s) items12 += (len[s] + 4095) >> 12;
-  int item_log2 = items12 < uint64_t(sm_count()) * 16 ? kMinItemLog2 : 12;
+  // work-item size: 2^13 floats (32 KB; items are claimed dynamically, so no
+  // wave quantisation to fit), halved while that leaves fewer items than
+  // resident warps. Sweeps (tools/scaling_probe.py, tools/kernel_times.py,
+  // 2^27..2^30 floats): fused map+reduce 2^12 and 2^13 within 1%; the
+  // read-only reduce needs 2^13 — at 2^12 its items finish so fast that the
+  // single claim counter saturates (0.90 ms vs 0.585 ms for 2^30 floats).
+  int item_log2 = 13;
+  while (item_log2 > kMinItemLog2) {
+    uint64_t items = 0;
+    for (uint64_t s = 0; s < nseg; ++s) items += (len[s] + (1ull << item_log2) - 1) >> item_log2;
+    if (items >= uint64_t(sm_count()) * 16) break;
+    --item_log2;
+  }
   if (const char* e = getenv("UCG_ITEM_LOG2")) {  // tuning override (tools/)
     const int L = atoi(e);
     if (L >= kMinItemLog2 && L <= kMaxItemLog2) item_log2 = L;

@@ -20,7 +20,7 @@ def _bits(t):
 
 # ---- map -------------------------------------------------------------------------
 
-@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 127, 4096, 1000003])
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 127, 4096, 1000003, (1 << 24) + 12345])
 def test_map_affine_bitexact(cuda, n):
     from paper_1505_01120_b200 import ops
 
