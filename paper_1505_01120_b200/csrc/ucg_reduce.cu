@@ -23,9 +23,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
-#include <utility>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -758,22 +755,6 @@ int reduce_cl(const T* const* elem_ptrs, uint64_t count, uint64_t len, const uin
 }  // namespace ucg
 
 using namespace ucg;
-
-namespace {
-// One 8-byte claim counter per (device, stream), zeroed on that stream before
-// each claimed-item launch: launches on one stream serialise on it, launches
-// on different streams never share it.
-unsigned long long* stream_counter(cudaStream_t st) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> ctrs;
-  int d = 0;
-  if (cudaGetDevice(&d) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  unsigned long long*& c = ctrs[{d, st}];
-  if (!c && cudaMalloc(&c, sizeof(unsigned long long)) != cudaSuccess) c = nullptr;
-  return c;
-}
-}  // namespace
 
 extern "C" {
 

@@ -6,8 +6,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ucg_common.cuh"
@@ -64,6 +66,17 @@ int check_device() {
                                    " is not compute capability 10.x (built for sm_100a only)");
   }
   return UCG_OK;
+}
+
+unsigned long long* stream_counter(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> ctrs;
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  unsigned long long*& c = ctrs[{d, st}];
+  if (!c && cudaMalloc(&c, sizeof(unsigned long long)) != cudaSuccess) c = nullptr;
+  return c;
 }
 
 int sm_count() {
