@@ -120,7 +120,9 @@ int ucg_fill_bytes_u8(uint8_t* out, uint64_t n, uint64_t seed, uint64_t first, v
 /* A segment = one partition's concatenated payload (ucores/engine.hpp:102,
  * Element::concat element.hpp:132-174) stored contiguously in a device buffer
  * at float offset begin[s] (multiple of 4) with len[s] floats. The table is
- * uploaded once (synchronously) and reused by every launch over that layout. */
+ * uploaded once (synchronously) on the current device and reused by every
+ * launch over that layout on that device; it also carries the launches'
+ * work-item counters, so it serves one launch at a time. */
 typedef struct ucg_segtab ucg_segtab;
 int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg, ucg_segtab** out);
 int ucg_segtab_destroy(ucg_segtab* t);
@@ -133,7 +135,8 @@ int ucg_segtab_scratch_floats(const ucg_segtab* t, uint64_t* n_out);
 
 /* axpb run() body over n floats: y[i] = fl(fl(a*x[i]) + b) (no FMA
  * contraction, bit-identical to the host executor). x, y 16-byte aligned;
- * y may equal x. */
+ * y may equal x. Large maps hand out 16 KB work items from a per-stream
+ * counter (a memset node precedes the kernel). */
 int ucg_map_affine_f32(const float* x, float* y, uint64_t n, float a, float b, void* stream);
 
 /* Fig-3 vectoradd body: c = a (op) b. */
@@ -148,7 +151,9 @@ int ucg_elementwise2_i64(const int64_t* a, const int64_t* b, int64_t* c, uint64_
 /* out[s] = pairing-tree reduction (engine.hpp:172-190 rule applied to the
  * elements of segment s; op SUM: a+b, MAX: std::max) of segment s of x.
  * Empty segment: +0.0f (SUM) / -inf (MAX). scratch: ucg_segtab_scratch_floats
- * floats of device memory. Bit-identical to the host psum/pmax kernels. */
+ * floats of device memory. Bit-identical to the host psum/pmax kernels.
+ * One launch (work items claimed from the table's counter, trees in the
+ * kernel's tail). */
 int ucg_segment_reduce_f32(const float* x, const ucg_segtab* t, int op, float* scratch,
                            float* out, void* stream);
 
@@ -174,15 +179,16 @@ int ucg_xchg_open(ucg_xchg* x, const void* all_handles);
 int ucg_xchg_error(const ucg_xchg* x, int* err_out); /* 1 if a peer never arrived (synchronous) */
 int ucg_xchg_destroy(ucg_xchg* x);
 
-/* mapCLPartition(psum|pmax) + reduceCL stage 2 in two launches: pass 1 over
- * the work items (optionally fused with the axpb map when y != NULL: y is
- * written), then one kernel that reduces each segment to `partials` and whose
- * last CTA runs the pairing tree over all partitions into `result` (device,
- * one float). With xchg != NULL that CTA first stores this rank's partials
- * into every peer's buffer over NVLink and waits for all ranks' epoch flags,
- * so every rank obtains the same, reference-ordered result with no separate
- * collective launch. A segment table / exchange must not be used by two
- * launches concurrently. */
+/* mapCLPartition(psum|pmax) + reduceCL stage 2 in ONE launch: the kernel
+ * streams the segments' work items (fused with the axpb map when y != NULL:
+ * y is written), then — in its tail, under a cooperative launch — reduces
+ * each segment to `partials` and runs the pairing tree over all partitions
+ * into `result` (device, one float). With xchg != NULL the last CTA first
+ * stores this rank's partials into every peer's buffer over NVLink and waits
+ * for all ranks' epoch flags, so every rank obtains the same,
+ * reference-ordered result with no separate collective launch. The table
+ * holds the launch's counters: a segment table / exchange must not be used
+ * by two launches concurrently (the calls on one stream serialise). */
 int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, float a, float b, int op,
                               float* scratch, float* partials, ucg_xchg* xchg, float* result, void* stream);
 
@@ -241,7 +247,9 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out,
 
 /* The wordcount kernel's run() over one chunk: flags[gid] = 1 iff bytes[gid]
  * is a word character and (gid == 0 or bytes[gid-1] is a delimiter: space,
- * tab, LF, CR — ucores/dataset.hpp:87-89), else 0. Device u8 arrays. */
+ * tab, LF, CR — ucores/dataset.hpp:87-89), else 0. Device u8 arrays.
+ * create_from_text chunks end on a delimiter, so one call over consecutive
+ * chunks equals the per-chunk calls. */
 int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* flags, void* stream);
 
 /* ------------------------------------------------------------------------ */
