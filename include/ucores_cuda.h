@@ -135,7 +135,7 @@ int ucg_segtab_scratch_floats(const ucg_segtab* t, uint64_t* n_out);
 
 /* axpb run() body over n floats: y[i] = fl(fl(a*x[i]) + b) (no FMA
  * contraction, bit-identical to the host executor). x, y 16-byte aligned;
- * y may equal x. Large maps hand out 16 KB work items from a per-stream
+ * y may equal x. Large maps hand out 16 KB work items from a per-launch
  * counter (a memset node precedes the kernel). */
 int ucg_map_affine_f32(const float* x, float* y, uint64_t n, float a, float b, void* stream);
 

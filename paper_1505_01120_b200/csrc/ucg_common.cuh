@@ -26,11 +26,11 @@ int check_device();  // UCG_OK when the current device is compute capability 10.
 int sm_count();      // SMs of the current device (cached per device)
 extern std::atomic<uint64_t> g_launches;
 
-// One 8-byte claim counter per (current device, stream) for kernels that hand
-// out work items dynamically; the caller zeroes it on `st` before each launch,
-// so launches on one stream serialise on it and different streams never
-// share it. Null if the allocation fails.
-unsigned long long* stream_counter(cudaStream_t st);
+// An 8-byte claim counter on the current device for one launch of a kernel
+// that hands out work items dynamically (the next slot of a per-device ring;
+// the caller zeroes it on its stream before the launch). Null if the ring
+// cannot be allocated.
+unsigned long long* claim_counter();
 
 // True the first time it is called on the current device for this flag word.
 // Kernel attributes (cudaFuncSetAttribute) are per device: a process driving

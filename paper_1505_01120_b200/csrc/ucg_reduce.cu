@@ -768,7 +768,7 @@ int ucg_map_affine_f32(const float* x, float* y, uint64_t n, float a, float b, v
   const uint64_t nitems = n / kItem;
   uint64_t done = 0;
   if (nitems >= uint64_t(sm_count()) * 16) {  // large maps: claimed 16 KB items
-    unsigned long long* ctr = stream_counter(st);
+    unsigned long long* ctr = claim_counter();
     if (!ctr) return fail(UCG_ERR_CUDA, "map: counter allocation failed");
     UCG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
     const unsigned grid = unsigned(std::min<uint64_t>((nitems + kWarps - 1) / kWarps, uint64_t(sm_count()) * 2));

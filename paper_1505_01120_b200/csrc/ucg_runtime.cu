@@ -6,10 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <map>
 #include <mutex>
 #include <string>
-#include <utility>
 #include <vector>
 
 #include "ucg_common.cuh"
@@ -68,15 +66,24 @@ int check_device() {
   return UCG_OK;
 }
 
-unsigned long long* stream_counter(cudaStream_t st) {
+unsigned long long* claim_counter() {
+  // a ring of 2^16 counters per device (512 KB): each launch takes the next
+  // slot, so concurrent launches (any streams) use distinct counters unless
+  // 65536 launches are in flight at once
+  constexpr uint64_t kSlots = 1u << 16;
   static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, unsigned long long*> ctrs;
+  static unsigned long long* ring[64] = {};
+  static uint64_t next[64] = {};
   int d = 0;
-  if (cudaGetDevice(&d) != cudaSuccess) return nullptr;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  unsigned long long*& c = ctrs[{d, st}];
-  if (!c && cudaMalloc(&c, sizeof(unsigned long long)) != cudaSuccess) c = nullptr;
-  return c;
+  if (!ring[d]) {
+    if (cudaMalloc(&ring[d], kSlots * sizeof(unsigned long long)) != cudaSuccess) {
+      ring[d] = nullptr;
+      return nullptr;
+    }
+  }
+  return ring[d] + (next[d]++ % kSlots);
 }
 
 int sm_count() {

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) k_word_flags(const uint8_t* __restrict__ 
 }
 
 // Claimed variant: a warp claims units of kClaim consecutive blocks (16 KB)
-// from a per-stream counter and walks them with the same prefetch.
+// from a per-launch counter and walks them with the same prefetch.
 template <int kWU, int kClaim>
 __global__ void __launch_bounds__(256) k_word_flags_claim(const uint8_t* __restrict__ in, uint8_t* __restrict__ flags,
                                                           uint64_t n16, unsigned long long* __restrict__ ctr) {
@@ -171,7 +171,7 @@ extern "C" int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* f
       const unsigned grid = unsigned(std::min<uint64_t>((warps + 7) / 8, uint64_t(sm_count()) * 8));
       k_word_flags<4><<<grid, 256, 0, st>>>(bytes, flags, n16);
     } else {
-      unsigned long long* ctr = stream_counter(st);
+      unsigned long long* ctr = claim_counter();
       if (!ctr) return fail(UCG_ERR_CUDA, "word flags: counter allocation failed");
       UCG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
       const unsigned grid = unsigned(std::min<uint64_t>((warps / 8 + 7) / 8 + 1, uint64_t(sm_count()) * 8));
