@@ -216,10 +216,18 @@ struct SobelMaps {
   CUtensorMap side;    // box {16 B, 66 rows}
 };
 
+// Where a buffer's tile lies: written by the issuing thread before the TMA
+// and published to the CTA by the buffer's mbarrier phase (the arrive has
+// release semantics), so only that thread runs the band search.
+struct TileInfo {
+  uint32_t b, rb, cb;
+};
+
 __device__ __forceinline__ void issue_tile(const SobelMaps* maps, const SobelTiles& p, uint32_t t, uint8_t* buf,
-                                           uint64_t* bar) {
+                                           uint64_t* bar, TileInfo* info) {
   uint32_t b, rb, cb;
   tile_of(p, t, b, rb, cb);
+  *info = TileInfo{b, rb, cb};
   const int x = int(cb) * kTW, y = int(p.in_row0[b] + rb * kTH);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)),
                "r"(kCenterBytes + 2 * kSideBytes) : "memory");
@@ -239,6 +247,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   __shared__ __align__(8) uint64_t full[2];
+  __shared__ TileInfo info[2];
   const int tid = threadIdx.x, cg = tid & 15, rg = tid >> 4;
   const SobelMaps* map = &maps;
   if (tid == 0) {
@@ -249,8 +258,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   __syncthreads();
   uint32_t it = 0;
   if (tid == 0) {
-    if (blockIdx.x < ntiles) issue_tile(map, p, blockIdx.x, smem, &full[0]);
-    if (blockIdx.x + gridDim.x < ntiles) issue_tile(map, p, blockIdx.x + gridDim.x, smem + kBufBytes, &full[1]);
+    if (blockIdx.x < ntiles) issue_tile(map, p, blockIdx.x, smem, &full[0], &info[0]);
+    if (blockIdx.x + gridDim.x < ntiles)
+      issue_tile(map, p, blockIdx.x + gridDim.x, smem + kBufBytes, &full[1], &info[1]);
   }
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const uint32_t bi = it & 1;
@@ -258,8 +268,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     asm volatile("{\n .reg .pred q;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n @!q bra W;\n}\n" ::"r"(
                      sa(&full[bi])), "r"((it >> 1) & 1)
                  : "memory");
-    uint32_t b, rb, cb;
-    tile_of(p, t, b, rb, cb);
+    const uint32_t b = info[bi].b, rb = info[bi].rb, cb = info[bi].cb;
     const uint32_t valid_rows = min(uint32_t(kTH), p.rows[b] - rb * kTH);
     const uint64_t col = uint64_t(cb) * kTW + cg * 16;
     const uint8_t* center = buf;
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     terms(i0 + 9, t0);
     emit(7, t1, t2, t0);
     __syncthreads();  // buffer bi fully read
-    if (tid == 0 && t + 2 * gridDim.x < ntiles) issue_tile(map, p, t + 2 * gridDim.x, buf, &full[bi]);
+    if (tid == 0 && t + 2 * gridDim.x < ntiles) issue_tile(map, p, t + 2 * gridDim.x, buf, &full[bi], &info[bi]);
   }
 }
 
