@@ -36,7 +36,7 @@ def test_wordcount_oracle_golden(golden):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", ["", "a", " ", "a b a", "  lead\ttrail  ", "x" * 40, "\r\n\t " * 9,
-                                  "random", "corpus"])
+                                  "random", "corpus", "all_bytes"])
 def test_word_flags_gpu_bitexact(cuda, case):
     import torch
 
@@ -47,6 +47,10 @@ def test_word_flags_gpu_bitexact(cuda, case):
         data = bytes(rng.choice(np.frombuffer(b"ab \t\n\rxyz", np.uint8), 100003).tolist())
     elif case == "corpus":
         data = O.corpus(5, 30000)
+    elif case == "all_bytes":  # every byte value next to every delimiter (the kernel's SWAR compare)
+        rng = np.random.default_rng(2)
+        pairs = bytes(b for v in range(256) for d in b" \t\n\r" for b in (v, d, v))
+        data = pairs + bytes(rng.integers(0, 256, 100003, dtype=np.uint8).tolist()) + bytes(range(256)) * 3
     else:
         data = case.encode()
     want = O.word_start_flags(data)
