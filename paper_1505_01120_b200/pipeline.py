@@ -219,6 +219,27 @@ class MapReducePipeline:
                                   xg, self.result)
         return self.result
 
+    def graph_step(self) -> torch.Tensor:
+        """step() replayed from a CUDA graph captured on first use (one GPU):
+        the kernel node and its launch attributes are fixed, so a replay costs
+        one cudaGraphLaunch instead of the Python/ctypes launch path. Sharded
+        pipelines keep step(): the peer exchange advances an epoch per launch."""
+        if self.world > 1:
+            return self.step()
+        if getattr(self, "_graph", None) is None:
+            self.step()  # warm: allocations and lazy library state outside the capture
+            torch.cuda.synchronize()
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    self.step()
+            torch.cuda.current_stream().wait_stream(side)
+            self._graph = g
+        self._graph.replay()
+        return self.result
+
     def exchange_error(self) -> int:
         """1 if a peer never published its partials (checked synchronously)."""
         import ctypes as C

@@ -309,6 +309,20 @@ def test_c2_small_golden(cuda, golden, fused):
         pipe.close()
 
 
+def test_graph_step_matches_eager(cuda, golden):
+    """The CUDA-graph replay of the one-kernel step gives the eager result."""
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    g = golden["c2_small"]
+    for op in ("sum", "max"):
+        pipe = MapReducePipeline([g["L"]] * g["P"], op=op, fused=True)
+        eager = O.f32_bits(pipe.step().cpu().numpy()[0])
+        for _ in range(3):
+            r = pipe.graph_step()
+        assert O.f32_bits(r.cpu().numpy()[0]) == eager == g["total_" + op]
+        pipe.close()
+
+
 @pytest.mark.slow
 def test_c2_full_size(cuda):
     """C2 at the BASELINE size (2^30 fp32, 64 partitions): size-independent checks."""
