@@ -15,9 +15,27 @@ from .capi import call, ptr, stream_handle, u64_array
 
 
 def _require_cuda(*ts) -> None:
+    """Every tensor handed to the C-ABI is a contiguous buffer on the current
+    CUDA device (the kernels index raw pointers and run on that device)."""
+    cur = None
     for t in ts:
-        if t is not None and not t.is_cuda:
+        if t is None:
+            continue
+        if not t.is_cuda:
             raise capi.DeviceUnavailable("tensor is not on a CUDA device (no CPU fallback)")
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous (the C-ABI takes raw pointers)")
+        if cur is None:
+            import torch
+
+            cur = torch.cuda.current_device()
+        if t.device.index != cur:
+            raise ValueError(f"tensor is on cuda:{t.device.index} but the current device is cuda:{cur}")
+
+
+def _dtype(t, want, name: str) -> None:
+    if t is not None and t.dtype != want:
+        raise TypeError(f"{name} must be {want}, got {t.dtype}")
 
 
 def fill_uniform_(out, seed: int, first: int = 0, stream=None):
@@ -36,6 +54,12 @@ def fill_bytes_(out, seed: int, first: int = 0, stream=None):
 def map_affine(x, y, a: float, b: float, n: int | None = None, stream=None):
     """axpb mapCL body (engine.hpp:54-85): y = fl(fl(a*x)+b)."""
     _require_cuda(x, y)
+    import torch
+
+    _dtype(x, torch.float32, "x")
+    _dtype(y, torch.float32, "y")
+    if (x.numel() if n is None else n) > min(x.numel(), y.numel()):
+        raise ValueError("n exceeds the buffers")
     call("ucg_map_affine_f32", ptr(x), ptr(y), x.numel() if n is None else n, a, b, stream_handle(stream))
     return y
 

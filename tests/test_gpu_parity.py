@@ -34,6 +34,23 @@ def test_map_affine_bitexact(cuda, n):
     assert np.array_equal(_bits(xd), O.map_affine(x, 0.3, -7.25).view(np.uint32))
 
 
+def test_ops_reject_bad_buffers(cuda):
+    """The C-ABI indexes raw pointers: non-contiguous, wrongly typed or
+    undersized tensors are refused before any launch."""
+    from paper_1505_01120_b200 import ops
+
+    x = torch.zeros(64, 4, device=cuda)
+    y = torch.zeros(64, 4, device=cuda)
+    with pytest.raises(ValueError):
+        ops.map_affine(x.t(), y, 2.0, 1.0)
+    with pytest.raises(TypeError):
+        ops.map_affine(x.double(), y, 2.0, 1.0)
+    with pytest.raises(ValueError):
+        ops.map_affine(x, y[:10], 2.0, 1.0, n=256)
+    with pytest.raises(Exception):
+        ops.map_affine(x.cpu(), y, 2.0, 1.0)
+
+
 # ---- partition reductions ----------------------------------------------------------
 
 SEG_LENS = [0, 1, 2, 3, 4, 5, 31, 127, 128, 129, 1023, 1024, 1025, 16383, 16384, 16385, 40000, 100003, 262144]
