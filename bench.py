@@ -251,8 +251,8 @@ def our_arm(args, world, rank, local):
         barrier()
         launches = capi.launch_count() - launches0
         result = float(pipe.result.item())
-        # timed region 2 (roofline): K launches of the dominant kernel pair
-        # (map+partition-reduce pass 1 + per-partition pass 2), one event pair each
+        # timed region 2 (roofline): K launches of the dominant kernel (the
+        # fused map + partition reduce, trees in its tail), one event pair each
         barrier()
         for i in range(k):
             ev[i][0].record()

@@ -11,9 +11,9 @@ at a 256-byte aligned float offset of one buffer (x and y share the layout).
 Sharding (SURVEY.md §8(e)): rank g of G holds partitions [gP/G, (g+1)P/G);
 the only exchange is of the per-partition partials, after which every rank
 runs the reference stage-2 tree over all P partials in partition order —
-bit-identical to one GPU. Default exchange "p2p": the finish kernel itself
-stores this rank's partials into every peer's buffer over NVLink (CUDA IPC
-mapped) and waits on epoch flags, so a step is two launches with no
+bit-identical to one GPU. Default exchange "p2p": the reduction kernel's
+tail stores this rank's partials into every peer's buffer over NVLink (CUDA
+IPC mapped) and waits on epoch flags, so a step is ONE launch with no
 collective; "nccl" uses torch.distributed all-gather + a tree launch.
 
 With fused=True the map and the partition reduction run as ONE kernel (read
@@ -108,8 +108,9 @@ class MapReducePipeline:
                  fused: bool = True, world: int = 1, rank: int = 0, device: torch.device | None = None,
                  seed_base: int = 1000, plant_max: bool = True, group=None, exchange: str = "p2p"):
         """exchange: how a sharded reduce_cl combines partials — "p2p" (the
-        finish kernel stores into peers' buffers over NVLink and waits on
-        epoch flags; no collective launch) or "nccl" (all-gather + tree)."""
+        reduction kernel's tail stores into peers' buffers over NVLink and
+        waits on epoch flags; no collective launch) or "nccl" (all-gather +
+        tree)."""
         self.P = len(part_lens)
         self.exchange = exchange
         self.part_lens = list(part_lens)
