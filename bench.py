@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-engine-e2e", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5", "wc"],
+    ap.add_argument("--workload", default="c2", choices=["c1", "c1lit", "c2", "c3", "c4", "c5", "wc"],
                     help="c2 (default) is the headline; the others are the remaining BASELINE configs")
     ap.add_argument("--cpu-sample-parts", type=int, default=4)
     return ap.parse_args()
@@ -76,6 +76,16 @@ def run_ref_harness(parts: int, part_len: int, steps: int, warmup: int, op: str,
         raise RuntimeError(f"{REF_HARNESS} missing (build it with `make -C oracle ref` where the reference exists)")
     cmd = [str(REF_HARNESS), "bench", "--parts", str(parts), "--part-len", str(part_len), "--threads",
            str(threads), "--steps", str(steps), "--warmup", str(warmup), "--op", op]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=1800).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def run_ref_harness_literal(n: int, parts: int) -> dict:
+    """The reference's one-task-per-element C1 literal chain (oracle/_ref)."""
+    if not REF_HARNESS.exists():
+        raise RuntimeError(f"{REF_HARNESS} missing (build it with `make -C oracle ref` where the reference exists)")
+    cmd = [str(REF_HARNESS), "bench-literal", "--n", str(n), "--parts", str(parts), "--threads",
+           str(os.cpu_count() or 1), "--steps", "1", "--warmup", "0"]
     out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=1800).stdout
     return json.loads(out.strip().splitlines()[-1])
 

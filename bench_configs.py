@@ -252,6 +252,53 @@ def run(args, world, rank, local):
                      {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s", "frac": per_gpu / peak,
                       "traffic": None, "peak_kind": "cuBLAS TF32 8192^3 measured in this run"},
                      cpu, {"workload": CONFIGS[4], "n": n, "partitions": P, "dtype": "tf32 (fp32 in/out, fp32 accumulate)"})
+    elif args.workload == "c1lit":
+        # the C1 literal form — 2^20 one-float elements — through
+        # the reference API: the GPU drop-in driver (one batched launch per wave)
+        # and the device-resident DeviceEngine, against the reference's
+        # one-task-per-element host path. An API-level, end-to-end number: host
+        # Elements in, one Element out, Dataset construction timed.
+        from paper_1505_01120_b200 import engine_capi
+
+        n, P = 1 << 20, 4
+        xd = torch.empty(n, dtype=torch.float32, device=dev)
+        ops.fill_uniform_(xd, 12345)
+        xh = xd.cpu().numpy()
+        runs, launches = {}, None
+        if rank == 0:
+            with B.ClockSampler(local) as clk:
+                for mode in ("device", "batched"):
+                    engine_capi.literal_f32(xh[:4096], P, mode=mode, gpus=1)  # warm: library and GPU state
+                    ts, r = [], None
+                    reps = max(3, min(k, 5))
+                    l0 = capi.launch_count()
+                    for _ in range(reps):
+                        r, sec = engine_capi.literal_f32(xh, P, mode=mode, gpus=1)
+                        ts.append(sec)
+                    if mode == "device":
+                        launches = (capi.launch_count() - l0) // reps
+                    runs[mode] = (statistics.median(ts), r)
+            rr = B.run_ref_harness_literal(n, P)
+            ref_s = statistics.median(rr["step_s"])
+            ref_bits = rr["result_bits"]
+            cpu = {"value": n / ref_s, "unit": "elements/s", "cores": rr["threads"], "kind": "reference",
+                   "sample": "the full literal workload: 2^20 one-float elements in 4 partitions, one map task per element"}
+            sec_d, r_d = runs["device"]
+            sec_b, r_b = runs["batched"]
+            import numpy as np
+
+            bits = lambda v: format(int(np.float32(v).view(np.uint32)), "08x")
+            match = bits(r_d) == bits(r_b) == ref_bits
+            line = _line(args, world, "c1lit", "C1 literal form: 2^20 one-float elements (SURVEY 8(f)3)",
+                         n / sec_d, "elements/s", sec_d * 1e3, launches, clk,
+                         {"value": n / sec_d, "unit": "elements/s", "h2d_bytes_per_step": 4 * n,
+                          "d2h_bytes_per_step": 4, "note": "the value itself is end to end (host Elements in)"},
+                         {"bound": "host", "achieved": None, "peak": None, "unit": None, "frac": None,
+                          "traffic": None, "note": "dominated by building 2^20 host Elements (timed in every arm)"},
+                         cpu, {"workload": "C1 literal: 2^20 fp32 one-float elements, 4 partitions",
+                               "dtype": "f32", "path": "ucores_b200::DeviceEngine via ucd_literal_f32",
+                               "seam_a_batched_elements_per_s": n / sec_b, "results_match_reference": match,
+                               "result_bits": bits(r_d)})
     elif args.workload == "wc":
         # WordCount word-start flags over create_from_text chunks.
         # Every chunk ends on a delimiter (dataset.hpp:94-112), so the flags of

@@ -51,6 +51,15 @@ int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts,
                      int gpus, int mode, float* y_out, float* partials_out, float* result_out,
                      double* seconds_out);
 
+/* The C1 literal form: n one-float elements x[i] in nparts
+ * partitions (create_dataset, ceiling-first), then the same chain as
+ * ucd_pipeline_f32. map_cl is one task per element in the reference; the GPU
+ * paths batch the wave (BATCHED) or keep the dataset in HBM (DEVICE).
+ * seconds_out: wall time from the host array to the result (Dataset
+ * construction included). */
+int ucd_literal_f32(const float* x, uint64_t n, uint64_t nparts, float a, float b, int op, int gpus, int mode,
+                    float* result_out, double* seconds_out);
+
 /* Monte-Carlo pi through Engine::map_cl(d, "pi") over `tasks` elements
  * {seed + t, samples split ceiling-first}: hits_out receives the total. */
 int ucd_pi(uint64_t samples, uint64_t tasks, uint64_t seed, int gpus, int64_t* hits_out, double* seconds_out);

@@ -858,6 +858,50 @@ int run_bench_workload(int argc, char** argv) {
   return 0;
 }
 
+// C1 literal form: n one-float elements in P partitions,
+// map_cl(axpb) -> map_cl_partition(p<op>) -> reduce_cl(<op>2); map_cl is one
+// task per element. Dataset construction is timed, as in ucd_literal_f32.
+int run_bench_literal(int argc, char** argv) {
+  std::size_t n = 1u << 18, P = 4;
+  unsigned threads = 1;
+  int steps = 1, warmup = 0;
+  std::string op = "sum";
+  for (int i = 2; i + 1 < argc; i += 2) {
+    std::string k = argv[i], v = argv[i + 1];
+    if (k == "--n") n = std::stoull(v);
+    else if (k == "--parts") P = std::stoull(v);
+    else if (k == "--threads") threads = static_cast<unsigned>(std::stoul(v));
+    else if (k == "--steps") steps = std::stoi(v);
+    else if (k == "--warmup") warmup = std::stoi(v);
+    else if (k == "--op") op = v;
+  }
+  KernelRegistry reg = make_registry(16, 16);
+  DirectDriver drv(reg, host_device(threads));
+  Engine eng(drv, reg);
+  std::vector<double> times;
+  float result = 0;
+  for (int s = 0; s < warmup + steps; ++s) {
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<Element> es;
+    es.reserve(n);
+    for (std::size_t i = 0; i < n; ++i) es.push_back(Element::f32({uniform01(12345, i)}));
+    Dataset x = create_dataset(std::move(es), P);
+    Element r = eng.reduce_cl(eng.map_cl_partition(eng.map_cl(x, "axpb"), "p" + op), op + "2");
+    auto t1 = std::chrono::steady_clock::now();
+    result = r.as_f32()[0];
+    if (s >= warmup) times.push_back(std::chrono::duration<double>(t1 - t0).count());
+  }
+  json out;
+  out["elements"] = n;
+  out["partitions"] = P;
+  out["threads"] = threads;
+  out["executor"] = threads <= 1 ? "host-seq" : "host-par";
+  out["step_s"] = times;
+  out["result_bits"] = hexf(result);
+  std::cout << out.dump() << std::endl;
+  return 0;
+}
+
 int run_bench(int argc, char** argv) {
   std::size_t P = 4, L = 1u << 24;
   unsigned threads = std::thread::hardware_concurrency();
@@ -917,6 +961,7 @@ int main(int argc, char** argv) {
     }
     if (mode == "bench") return run_bench(argc, argv);
     if (mode == "bench-workload") return run_bench_workload(argc, argv);
+    if (mode == "bench-literal") return run_bench_literal(argc, argv);
   } catch (const std::exception& e) {
     std::cerr << "ref_harness: " << e.what() << std::endl;
     return 1;

@@ -28,6 +28,9 @@ def load() -> C.CDLL:
         L.ucd_pipeline_f32.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64, C.c_float, C.c_float, C.c_int,
                                        C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_float),
                                        C.POINTER(C.c_double)]
+        L.ucd_literal_f32.restype = C.c_int
+        L.ucd_literal_f32.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_float, C.c_float, C.c_int, C.c_int,
+                                      C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_double)]
         L.ucd_pi.restype = C.c_int
         L.ucd_pi.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         _lib = L
@@ -53,6 +56,16 @@ def pipeline_f32(x: np.ndarray, part_lens, a: float = 2.0, b: float = 1.0, op: s
                                    y.ctypes.data if want_y else None, partials.ctypes.data, C.byref(res),
                                    C.byref(sec)))
     return y, partials, np.float32(res.value), sec.value
+
+
+def literal_f32(x: np.ndarray, parts: int, a: float = 2.0, b: float = 1.0, op: str = "sum", gpus: int = -1,
+                mode: str = "device"):
+    """C1 literal form: one-float elements; (result, seconds) of the same chain."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    res, sec = C.c_float(0), C.c_double(0)
+    _check(load().ucd_literal_f32(x.ctypes.data, x.size, parts, a, b, capi.OPS[op], gpus, MODE[mode], C.byref(res),
+                                  C.byref(sec)))
+    return np.float32(res.value), sec.value
 
 
 def pi(samples: int, tasks: int, seed: int, gpus: int = -1):

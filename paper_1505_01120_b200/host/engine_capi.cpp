@@ -126,6 +126,48 @@ int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts,
   });
 }
 
+int ucd_literal_f32(const float* x, uint64_t n, uint64_t nparts, float a, float b, int op, int gpus, int mode,
+                    float* result_out, double* seconds_out) {
+  return guarded([&] {
+    using namespace ucores;
+    using namespace ucores_b200;
+    KernelRegistry reg;
+    DeviceOpRegistry ops;
+    WorkloadParams p;
+    p.a = a;
+    p.b = b;
+    register_workload(reg, ops, p);
+    const std::string pk = op == 1 ? "pmax" : "psum", rk = op == 1 ? "max2" : "sum2";
+    auto dataset = [&] {
+      std::vector<Element> es;
+      es.reserve(n);
+      for (uint64_t i = 0; i < n; ++i) es.push_back(Element::f32({x[i]}));
+      return create_dataset(std::move(es), nparts);
+    };
+    Element r;
+    std::chrono::steady_clock::time_point t0, t1;
+    if (mode == UCD_MODE_DEVICE) {
+      DeviceEngine de(p, gpus);
+      t0 = std::chrono::steady_clock::now();
+      Dataset d = dataset();
+      r = de.reduce_cl(de.map_cl_partition(de.map_cl(de.upload(d), "axpb"), pk), rk);
+      t1 = std::chrono::steady_clock::now();
+    } else {
+      GpuClusterDriver::Options opt;
+      opt.max_gpus = gpus;
+      opt.mode = mode == UCD_MODE_PER_TASK ? GpuClusterDriver::Mode::PerTask : GpuClusterDriver::Mode::Batched;
+      GpuClusterDriver drv(reg, ops, opt);
+      Engine eng(drv, reg);
+      t0 = std::chrono::steady_clock::now();
+      Dataset d = dataset();
+      r = eng.reduce_cl(eng.map_cl_partition(eng.map_cl(d, "axpb"), pk), rk);
+      t1 = std::chrono::steady_clock::now();
+    }
+    if (seconds_out) *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+    if (result_out) *result_out = r.as_f32()[0];
+  });
+}
+
 int ucd_pi(uint64_t samples, uint64_t tasks, uint64_t seed, int gpus, int64_t* hits_out, double* seconds_out) {
   return guarded([&] {
     using namespace ucores;

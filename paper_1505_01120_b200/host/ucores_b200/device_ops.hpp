@@ -102,6 +102,54 @@ inline std::vector<std::uint64_t> pack_offsets(const std::vector<std::uint64_t>&
 
 inline int op_code(kernels::ReduceOp op) { return op == kernels::ReduceOp::Max ? UCG_OP_MAX : UCG_OP_SUM; }
 
+// Many small payloads (a wave of one-float elements) move as ONE DMA through
+// the GPU's pinned staging; large ones go directly, one copy each.
+inline bool pack_pieces(std::size_t count, std::uint64_t bytes) {
+  return count > 8 && bytes / count < (256u << 10);
+}
+
+// Host -> device: piece i lands at element offset off[i] of dst.
+template <class T>
+void upload_pieces(Gpu& g, T* dst, const std::vector<std::span<const T>>& in, const std::vector<std::uint64_t>& off,
+                   int stage_slot = 0) {
+  if (in.empty()) return;
+  std::uint64_t bytes = 0;
+  for (const auto& v : in) bytes += v.size_bytes();
+  if (pack_pieces(in.size(), bytes)) {
+    const std::uint64_t extent = off.back() + in.back().size();
+    T* h = static_cast<T*>(g.host_stage(stage_slot, std::max<std::uint64_t>(extent, 1) * sizeof(T)));
+    for (std::size_t i = 0; i < in.size(); ++i)
+      if (!in[i].empty()) std::memcpy(h + off[i], in[i].data(), in[i].size_bytes());
+    g.h2d(dst, h, extent * sizeof(T));
+  } else {
+    for (std::size_t i = 0; i < in.size(); ++i) g.h2d(dst + off[i], in[i].data(), in[i].size_bytes());
+  }
+}
+
+// Device -> host: piece i (sizes[i] elements at offset off[i] of src) into its
+// own vector. Synchronises the GPU's stream.
+template <class T>
+std::vector<std::vector<T>> download_pieces(Gpu& g, const T* src, const std::vector<std::uint64_t>& sizes,
+                                            const std::vector<std::uint64_t>& off, int stage_slot = 1) {
+  std::vector<std::vector<T>> out(sizes.size());
+  std::uint64_t bytes = 0;
+  for (std::uint64_t n : sizes) bytes += n * sizeof(T);
+  if (!sizes.empty() && pack_pieces(sizes.size(), bytes)) {
+    const std::uint64_t extent = off.back() + sizes.back();
+    T* h = static_cast<T*>(g.host_stage(stage_slot, std::max<std::uint64_t>(extent, 1) * sizeof(T)));
+    g.d2h(h, src, extent * sizeof(T));
+    g.sync();
+    for (std::size_t i = 0; i < sizes.size(); ++i) out[i].assign(h + off[i], h + off[i] + sizes[i]);
+  } else {
+    for (std::size_t i = 0; i < sizes.size(); ++i) {
+      out[i].resize(sizes[i]);
+      g.d2h(out[i].data(), src + off[i], sizes[i] * sizeof(T));
+    }
+    g.sync();
+  }
+  return out;
+}
+
 }  // namespace detail
 
 namespace device_ops {
@@ -121,16 +169,11 @@ inline DeviceOp affine_f32(float a, float b) {
     const auto off = detail::pack_offsets(sizes, 64, &total);
     float* x = static_cast<float*>(g.scratch(0).ensure(total * 4));
     float* y = static_cast<float*>(g.scratch(1).ensure(total * 4));
-    for (std::size_t i = 0; i < in.size(); ++i) g.h2d(x + off[i], in[i].data(), sizes[i] * 4);
+    detail::upload_pieces(g, x, in, off);
     check(ucg_map_affine_f32(x, y, total, a, b, g.stream()));
     std::vector<ucores::Element> out;
     out.reserve(in.size());
-    for (std::size_t i = 0; i < in.size(); ++i) {
-      std::vector<float> v(sizes[i]);
-      g.d2h(v.data(), y + off[i], sizes[i] * 4);
-      out.push_back(ucores::Element::f32(std::move(v)));
-    }
-    g.sync();
+    for (auto& v : detail::download_pieces<float>(g, y, sizes, off)) out.push_back(ucores::Element::f32(std::move(v)));
     return out;
   };
   op.run_phase = [a, b](Gpu& g, ucores::KernelContext& ctx) {
@@ -161,7 +204,7 @@ inline DeviceOp partition_reduce_f32(kernels::ReduceOp rop) {
     std::uint64_t total = 0;
     const auto off = detail::pack_offsets(sizes, 64, &total);
     float* x = static_cast<float*>(g.scratch(0).ensure(total * 4));
-    for (std::size_t i = 0; i < in.size(); ++i) g.h2d(x + off[i], in[i].data(), sizes[i] * 4);
+    detail::upload_pieces(g, x, in, off);
     ucg_segtab* tab = nullptr;
     check(ucg_segtab_create(off.data(), sizes.data(), sizes.size(), &tab));
     std::uint64_t nscratch = 0;
@@ -223,20 +266,15 @@ std::vector<ucores::Element> elementwise_tasks(Gpu& g, TaskBatch tasks, int code
   T* a = static_cast<T*>(g.scratch(0).ensure(total * sizeof(T)));
   T* b = static_cast<T*>(g.scratch(1).ensure(total * sizeof(T)));
   T* c = static_cast<T*>(g.scratch(2).ensure(total * sizeof(T)));
-  for (std::size_t i = 0; i < sizes.size(); ++i) {
-    g.h2d(a + off[i], A[i].data(), sizes[i] * sizeof(T));
-    g.h2d(b + off[i], B[i].data(), sizes[i] * sizeof(T));
-  }
+  detail::upload_pieces(g, a, A, off, 0);
+  detail::upload_pieces(g, b, B, off, 2);
   if constexpr (std::is_same_v<T, float>) check(ucg_elementwise2_f32(a, b, c, total, code, g.stream()));
   else check(ucg_elementwise2_i64(a, b, c, total, g.stream()));
   std::vector<ucores::Element> out;
-  for (std::size_t i = 0; i < sizes.size(); ++i) {
-    std::vector<T> v(sizes[i]);
-    g.d2h(v.data(), c + off[i], sizes[i] * sizeof(T));
+  for (auto& v : detail::download_pieces<T>(g, c, sizes, off)) {
     if constexpr (std::is_same_v<T, float>) out.push_back(ucores::Element::f32(std::move(v)));
     else out.push_back(ucores::Element::i64(std::move(v)));
   }
-  g.sync();
   return out;
 }
 
@@ -332,16 +370,12 @@ inline DeviceOp sobel(std::size_t width) {
     const auto out_off = detail::pack_offsets(out_sz, 16, &tout);
     std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(tin));
     std::uint8_t* dout = static_cast<std::uint8_t*>(g.scratch(1).ensure(tout));
-    for (std::size_t i = 0; i < in.size(); ++i) g.h2d(din + in_off[i], in[i].data(), in_sz[i]);
+    detail::upload_pieces(g, din, in, in_off);
     check(ucg_sobel_bands_u8(din, in_off.data(), dout, out_off.data(), rows.data(), rows.size(), width,
                              g.stream()));
     std::vector<ucores::Element> out;
-    for (std::size_t i = 0; i < in.size(); ++i) {
-      std::vector<std::uint8_t> v(out_sz[i]);
-      g.d2h(v.data(), dout + out_off[i], out_sz[i]);
+    for (auto& v : detail::download_pieces<std::uint8_t>(g, dout, out_sz, out_off))
       out.push_back(ucores::Element::bytes(std::move(v)));
-    }
-    g.sync();
     return out;
   };
   op.run_phase = [width](Gpu& g, ucores::KernelContext& ctx) {

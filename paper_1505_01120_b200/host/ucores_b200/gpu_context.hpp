@@ -94,11 +94,28 @@ class Gpu {
   Gpu(const Gpu&) = delete;
   Gpu& operator=(const Gpu&) = delete;
   ~Gpu() {
+    for (Stage& st : stages_)
+      if (st.ptr) ucg_host_free(st.ptr);
     if (stream_) {
       DeviceGuard guard;
       ucg_set_device(ordinal_);
       ucg_stream_destroy(stream_);
     }
+  }
+
+  /// Pinned host staging (grow-only) by slot: packs many small payloads into
+  /// one DMA. A slot's contents are in use until the next sync().
+  void* host_stage(int slot, std::uint64_t bytes) {
+    if (slot >= static_cast<int>(stages_.size())) stages_.resize(slot + 1);
+    Stage& st = stages_[slot];
+    if (st.bytes < bytes) {
+      if (st.ptr) ucg_host_free(st.ptr);
+      st.ptr = nullptr;
+      st.bytes = 0;
+      check(ucg_host_alloc(&st.ptr, bytes), "run");
+      st.bytes = bytes;
+    }
+    return st.ptr;
   }
 
   void bind() const { check(ucg_set_device(ordinal_), "run"); }
@@ -119,9 +136,14 @@ class Gpu {
   void d2h(void* dst, const void* src, std::uint64_t bytes) { check(ucg_memcpy_d2h(dst, src, bytes, stream_)); }
 
  private:
+  struct Stage {
+    void* ptr = nullptr;
+    std::uint64_t bytes = 0;
+  };
   int ordinal_;
   void* stream_ = nullptr;
   std::vector<DeviceBuffer> scratch_;
+  std::vector<Stage> stages_;
   std::mutex mu_;
 };
 
