@@ -420,19 +420,27 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
-  uint64_t item = warp;
-  while (item < p.nitems) {
-    // dynamic: the next item index is claimed now and consumed after this one
+  // A claim covers kPer consecutive items: one for the read+write map stream,
+  // two for the read-only reduction, whose items finish twice as fast and
+  // would otherwise saturate the single claim counter.
+  constexpr uint64_t kPer = kMap ? 1 : 2;
+  uint64_t unit = warp;
+  while (unit * kPer < p.nitems) {
+    // dynamic: the next unit is claimed now and consumed after this one
     uint32_t claim = 0;
     if (p.dynamic && lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
-    const uint32_t s = p.item_seg[item];
-    const uint64_t blk = item - p.first_item[s];
-    const uint64_t off = p.begin[s] + (blk << p.item_log2);
-    const int64_t item_floats = int64_t(1) << p.item_log2;
-    const int64_t valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
-    const float r = work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
-    if (lane == 0) p.partial[item] = r;
-    item = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : item + nwarps;
+#pragma unroll 1
+    for (uint64_t item = unit * kPer; item < umin((unit + 1) * kPer, p.nitems); ++item) {
+      const uint32_t s = p.item_seg[item];
+      const uint64_t blk = item - p.first_item[s];
+      const uint64_t off = p.begin[s] + (blk << p.item_log2);
+      const int64_t item_floats = int64_t(1) << p.item_log2;
+      const int64_t valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
+      const float r =
+          work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
+      if (lane == 0) p.partial[item] = r;
+    }
+    unit = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : unit + nwarps;
   }
   if (!p.finish) return;
   __shared__ TreeSmem sm;

@@ -288,13 +288,13 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if (int rc = check_device()) return rc;
   if (nseg && (!begin || !len)) return fail(UCG_ERR_ARG, "begin/len is null");
   if (nseg >= (1ull << 32)) return fail(UCG_ERR_ARG, "too many segments");
-  // work-item size: 2^13 floats (32 KB; items are claimed dynamically, so no
+  // work-item size: 2^12 floats (16 KB; items are claimed dynamically, so no
   // wave quantisation to fit), halved while that leaves fewer items than
   // resident warps. Sweeps (tools/scaling_probe.py, tools/kernel_times.py,
-  // 2^27..2^30 floats): fused map+reduce 2^12 and 2^13 within 1%; the
-  // read-only reduce needs 2^13 — at 2^12 its items finish so fast that the
-  // single claim counter saturates (0.90 ms vs 0.585 ms for 2^30 floats).
-  int item_log2 = 13;
+  // 2^27..2^30 floats): the fused map+reduce is best at 2^12 (smaller last
+  // items at 8-GPU shard sizes); the read-only reduce claims two items per
+  // atomic, since one claim per 2^12 items saturates the counter.
+  int item_log2 = 12;
   while (item_log2 > kMinItemLog2) {
     uint64_t items = 0;
     for (uint64_t s = 0; s < nseg; ++s) items += (len[s] + (1ull << item_log2) - 1) >> item_log2;
