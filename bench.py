@@ -349,15 +349,15 @@ def our_arm(args, world, rank, local):
             _, _, r_eng, sec = engine_capi.pipeline_f32(xs, pipe.local_lens, op=args.op, want_y=False)
             engine_e2e = {"value": n_total / sec, "unit": UNIT, "seconds": sec,
                           "path": "ucores::Engine map_cl/map_cl_partition/reduce_cl + GpuClusterDriver (seam A), "
-                                  "host Elements in, Element out (Dataset construction timed)",
+                                  "from a built host Dataset to the result Element (as the reference arm)",
                           "result_matches": bool(np.float32(r_eng) == np.float32(result))}
             engine_capi.pipeline_f32(xs[:1 << 20], [1 << 20], op=args.op, want_y=False, mode="device")  # warm
             _, _, r_dev, sec_d = engine_capi.pipeline_f32(xs, pipe.local_lens, op=args.op, want_y=False,
                                                           mode="device")
             engine_e2e["device_engine"] = {
                 "value": n_total / sec_d, "unit": UNIT, "seconds": sec_d,
-                "path": "ucores_b200::DeviceEngine (device_dataset.hpp): Dataset upload from pageable host "
-                        "Elements, map_cl/map_cl_partition/reduce_cl in HBM, one Element back",
+                "path": "ucores_b200::DeviceEngine (device_dataset.hpp): upload of the built host Dataset "
+                        "(pinned staging), map_cl/map_cl_partition/reduce_cl in HBM, one Element back",
                 "result_matches": bool(np.float32(r_dev) == np.float32(result))}
             del xs
         except Exception as e:  # reported, not hidden

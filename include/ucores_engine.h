@@ -45,8 +45,9 @@ const char* ucd_last_error(void);
  *   r = reduce_cl(ps, "sum2"|"max2")
  * y_out (nullable, sum(part_lens) floats) receives the collected y,
  * partials_out (nullable, nparts) the psum/pmax dataset, result_out the
- * reduced value. seconds_out: wall time from host arrays to the result
- * (Dataset construction included). gpus <= 0: every visible GPU. */
+ * reduced value. seconds_out: wall time from the built host Dataset to the
+ * result Element (the reference arm times its Engine the same way). gpus <= 0:
+ * every visible GPU. */
 int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts, float a, float b, int op,
                      int gpus, int mode, float* y_out, float* partials_out, float* result_out,
                      double* seconds_out);
