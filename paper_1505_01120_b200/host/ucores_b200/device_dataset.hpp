@@ -461,6 +461,9 @@ class DeviceEngine {
       }
     }
     DeviceDataset out = allocate(std::move(parts));
+    // temporaries live until every GPU's stream is drained (sync_all below),
+    // so the GPUs run concurrently and no block returns to the pool early
+    std::vector<std::shared_ptr<GpuAlloc>> keep;
     for (std::size_t g = 0; g < gpus_.size(); ++g) {
       const std::vector<Unit> units = units_of(d, g, per_partition);
       if (units.empty()) continue;
@@ -481,7 +484,7 @@ class DeviceEngine {
         std::vector<std::size_t> realign;  // units whose floats are not 16-byte aligned
         for (std::size_t i = 0; i < units.size(); ++i)
           if (begin[i] % 4) realign.push_back(i);
-        std::shared_ptr<GpuAlloc> tmp;
+        std::shared_ptr<GpuAlloc> tmp;  // kept alive through `keep`
         const float* base = reinterpret_cast<const float*>(ib);
         if (!realign.empty()) {  // map_cl over packed elements: copy them to aligned segments first
           std::uint64_t total = 0;
@@ -494,16 +497,20 @@ class DeviceEngine {
             at += (len[i] + 63) / 64 * 64;
           }
           base = reinterpret_cast<const float*>(tmp->at(0));
+          keep.push_back(tmp);
         }
         ucg_segtab* tab = segtab(g, begin, len);
         std::uint64_t nscratch = 0;
         check(ucg_segtab_scratch_floats(tab, &nscratch));
-        GpuAlloc scratch(pool_, gpu.ordinal(), nscratch * 4), vals(pool_, gpu.ordinal(), units.size() * 4);
+        auto scratch = std::make_shared<GpuAlloc>(pool_, gpu.ordinal(), nscratch * 4);
+        auto vals = std::make_shared<GpuAlloc>(pool_, gpu.ordinal(), units.size() * 4);
+        keep.push_back(scratch);
+        keep.push_back(vals);
         check(ucg_segment_reduce_f32(base, tab, kernel == "pmax" ? UCG_OP_MAX : UCG_OP_SUM,
-                                     reinterpret_cast<float*>(scratch.at(0)), reinterpret_cast<float*>(vals.at(0)), st));
+                                     reinterpret_cast<float*>(scratch->at(0)), reinterpret_cast<float*>(vals->at(0)),
+                                     st));
         for (std::size_t i = 0; i < units.size(); ++i)
-          check(ucg_memcpy_d2d(ob + ounits[i].in_off, vals.at(i * 4), 4, st));
-        check(ucg_stream_synchronize(st));  // scratch / table / tmp are freed on return
+          check(ucg_memcpy_d2d(ob + ounits[i].in_off, vals->at(i * 4), 4, st));
       } else if (kernel == "sobel") {
         std::vector<std::uint64_t> in_off, out_off, rows;
         for (std::size_t i = 0; i < units.size(); ++i) {
@@ -522,13 +529,15 @@ class DeviceEngine {
           seeds[i] = static_cast<std::uint64_t>(params[2 * i]);
           samples[i] = static_cast<std::uint64_t>(params[2 * i + 1]);
         }
-        GpuAlloc hits(pool_, gpu.ordinal(), units.size() * 8);
-        check(ucg_pi_hits(seeds.data(), samples.data(), units.size(), reinterpret_cast<std::int64_t*>(hits.at(0)), st));
+        auto hits = std::make_shared<GpuAlloc>(pool_, gpu.ordinal(), units.size() * 8);
+        keep.push_back(hits);
+        check(ucg_pi_hits(seeds.data(), samples.data(), units.size(), reinterpret_cast<std::int64_t*>(hits->at(0)),
+                          st));
         for (std::size_t i = 0; i < units.size(); ++i) {
-          check(ucg_memcpy_d2d(ob + ounits[i].in_off, hits.at(i * 8), 8, st));
+          check(ucg_memcpy_d2d(ob + ounits[i].in_off, hits->at(i * 8), 8, st));
+          // pageable source: staged before the call returns, so `samples` may go
           check(ucg_memcpy_h2d(ob + ounits[i].in_off + 8, &samples[i], 8, st));
         }
-        check(ucg_stream_synchronize(st));
       } else {  // matmul
         for (std::size_t i = 0; i < units.size(); ++i) {
           const float* a = reinterpret_cast<const float*>(ib + units[i].in_off);

@@ -525,13 +525,22 @@ int main() {
     auto t0 = std::chrono::steady_clock::now();
     DeviceDataset dx = de.upload(x);
     auto t1 = std::chrono::steady_clock::now();
-    Element rd = de.reduce_cl(de.map_cl_partition(de.map_cl(dx, "axpb"), "psum"), "sum2");
+    DeviceDataset dy = de.map_cl(dx, "axpb");
+    auto ta = std::chrono::steady_clock::now();
+    DeviceDataset dp = de.map_cl_partition(dy, "psum");
+    auto tb = std::chrono::steady_clock::now();
+    Element rd = de.reduce_cl(dp, "sum2");
     auto t2 = std::chrono::steady_clock::now();
     Element rh = eh.reduce_cl(eh.map_cl_partition(eh.map_cl(x, "axpb"), "psum"), "sum2");
     EXPECT(rd == rh, "sum bitwise vs host Engine");
-    std::printf("  device engine: upload %.1f ms, chain %.2f ms\n",
-                std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                std::chrono::duration<double, std::milli>(t2 - t1).count());
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::printf("  device engine: upload %.1f ms, chain %.2f ms (map_cl %.2f, map_cl_partition %.2f, reduce_cl %.2f)\n",
+                ms(t0, t1), ms(t1, t2), ms(t1, ta), ms(ta, tb), ms(tb, t2));
+    auto t3 = std::chrono::steady_clock::now();
+    Element rd2 = de.reduce_cl(de.map_cl_partition(de.map_cl(dx, "axpb"), "psum"), "sum2");
+    auto t4 = std::chrono::steady_clock::now();
+    EXPECT(rd2 == rh, "repeat chain bitwise");
+    std::printf("  device engine: repeated chain %.2f ms\n", ms(t3, t4));
   });
 
   std::printf("RESULT pass=%d fail=%d\n", g_pass, g_fail);
