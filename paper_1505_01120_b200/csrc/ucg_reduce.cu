@@ -588,23 +588,71 @@ struct F32MaxE {
   static __device__ __forceinline__ float apply(float a, float b) { return (a < b) ? b : a; }
 };
 
-constexpr int kMaxParts = 4096;  // per launch (host splits larger trees)
+// reduce_cl over vector elements, in two launches:
+//  stage 1 (engine.hpp:144-170): every non-empty partition's elements folded
+//    left to right, all partitions and lanes in parallel —
+//    short vectors (len < 32): one WARP per (partition, lane): the lanes load
+//      32 consecutive elements' values (the next 32 in flight) and lane 0's
+//      fold consumes them in order through shuffles, so a chain of 2^18
+//      one-float elements runs at shuffle + add latency, not load latency;
+//    long vectors: one thread per (partition, lane) with loads 8 ahead;
+//  stage 2 (engine.hpp:172-190): one thread per lane, the pairing tree over
+//    the partition partials in partition order (binary-counter stack of
+//    aligned subtrees, folded right to left).
+constexpr int kMaxParts = 4096;  // stage-2 stack depth 13
 
-// One thread per lane j. part_first[p]..part_first[p+1]: element range of the
-// p-th NON-EMPTY partition (nonempty entries). Stage 1 folds left to right,
-// stage 2 merges partials with a binary-counter stack (aligned subtrees),
-// then folds the stack right to left — the pairing tree with promotion.
 template <class T, class Op>
-__global__ void __launch_bounds__(128) k_reduce_cl(const T* const* __restrict__ elems, const uint64_t* __restrict__ part_first,
-                                                   uint64_t nonempty, uint64_t len, T* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_fold_warp(const T* const* __restrict__ elems,
+                                                   const uint64_t* __restrict__ part_first, uint64_t nonempty,
+                                                   uint64_t len, T* __restrict__ partials) {
+  const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nonempty * len) return;
+  const uint64_t k = w / len, j = w % len;
+  const uint64_t e0 = part_first[k], e1 = part_first[k + 1];
+  T acc = elems[e0][j];
+  uint64_t base = e0 + 1;
+  T v = base + lane < e1 ? elems[base + lane][j] : T{};
+  while (base < e1) {
+    const uint64_t nb = base + 32;
+    const T nv = nb + lane < e1 ? elems[nb + lane][j] : T{};  // next batch in flight
+    const int cnt = int(umin(32, e1 - base));
+    for (int i = 0; i < cnt; ++i) acc = Op::apply(acc, __shfl_sync(0xffffffffu, v, i));
+    v = nv;
+    base = nb;
+  }
+  if (lane == 0) partials[k * len + j] = acc;
+}
+
+template <class T, class Op>
+__global__ void __launch_bounds__(128) k_fold_thread(const T* const* __restrict__ elems,
+                                                     const uint64_t* __restrict__ part_first, uint64_t nonempty,
+                                                     uint64_t len, T* __restrict__ partials) {
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nonempty * len) return;
+  const uint64_t k = t / len, j = t % len;
+  const uint64_t e0 = part_first[k], e1 = part_first[k + 1];
+  T acc = elems[e0][j];
+  uint64_t e = e0 + 1;
+  for (; e + 8 <= e1; e += 8) {
+    T v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = elems[e + i][j];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc = Op::apply(acc, v[i]);
+  }
+  for (; e < e1; ++e) acc = Op::apply(acc, elems[e][j]);
+  partials[k * len + j] = acc;
+}
+
+template <class T, class Op>
+__global__ void __launch_bounds__(128) k_stage2(const T* __restrict__ partials, uint64_t nonempty, uint64_t len,
+                                                T* __restrict__ out) {
   const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= len) return;
   T stk[13];  // nonempty <= 4096 -> depth <= 12
-  uint64_t k = 0;
-  for (; k < nonempty; ++k) {
-    uint64_t e = part_first[k];
-    T acc = elems[e][j];
-    for (++e; e < part_first[k + 1]; ++e) acc = Op::apply(acc, elems[e][j]);
+  for (uint64_t k = 0; k < nonempty; ++k) {
+    T acc = partials[k * len + j];
     int lvl = 0;
 #pragma unroll 1
     while ((k >> lvl) & 1) {
@@ -749,13 +797,24 @@ int reduce_cl(const T* const* elem_ptrs, uint64_t count, uint64_t len, const uin
   if (nonempty > kMaxParts) return fail(UCG_ERR_ARG, "more than 4096 non-empty partitions");
   if (len == 0) return UCG_OK;
   uint64_t* d_first = nullptr;
+  T* d_part = nullptr;
   UCG_CUDA(cudaMallocAsync(&d_first, first.size() * 8, st));
+  UCG_CUDA(cudaMallocAsync(&d_part, nonempty * len * sizeof(T), st));
+  // (the pageable-source copy is staged before cudaMemcpyAsync returns)
   UCG_CUDA(cudaMemcpyAsync(d_first, first.data(), first.size() * 8, cudaMemcpyHostToDevice, st));
-  const unsigned grid = unsigned((len + 127) / 128);
-  k_reduce_cl<T, Op><<<grid, 128, 0, st>>>(elem_ptrs, d_first, nonempty, len, out);
+  const uint64_t chains = nonempty * len;
+  if (len < 32) {
+    const unsigned grid = unsigned((chains * 32 + 255) / 256);
+    k_fold_warp<T, Op><<<grid, 256, 0, st>>>(elem_ptrs, d_first, nonempty, len, d_part);
+  } else {
+    const unsigned grid = unsigned((chains + 127) / 128);
+    k_fold_thread<T, Op><<<grid, 128, 0, st>>>(elem_ptrs, d_first, nonempty, len, d_part);
+  }
   UCG_LAUNCHED();
-  // (the pageable-source copy above is staged before cudaMemcpyAsync returns)
+  k_stage2<T, Op><<<unsigned((len + 127) / 128), 128, 0, st>>>(d_part, nonempty, len, out);
+  UCG_LAUNCHED();
   UCG_CUDA(cudaFreeAsync(d_first, st));
+  UCG_CUDA(cudaFreeAsync(d_part, st));
   return UCG_OK;
 }
 

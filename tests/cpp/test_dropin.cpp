@@ -511,6 +511,15 @@ int main() {
       }
       std::printf("  literal 2^%d elements: device chain incl. upload %.2f ms\n", int(std::log2(double(n))),
                   std::chrono::duration<double, std::milli>(t1 - t0).count());
+      // reduce_cl straight over the one-float elements: n-1 ReducePair tasks
+      // in the reference (stage-1 folds of 2^18 elements per partition)
+      DeviceDataset dx = de.upload(x);
+      auto t2 = std::chrono::steady_clock::now();
+      Element rr = de.reduce_cl(dx, "sum2");
+      auto t3 = std::chrono::steady_clock::now();
+      if (n <= (1u << 16)) EXPECT(rr == eh.reduce_cl(x, "sum2"), "literal reduce_cl bitwise vs host Engine");
+      std::printf("  literal 2^%d elements: device reduce_cl %.2f ms\n", int(std::log2(double(n))),
+                  std::chrono::duration<double, std::milli>(t3 - t2).count());
     }
   });
 

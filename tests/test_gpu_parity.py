@@ -235,6 +235,35 @@ def _reduce_cl_gpu(cuda, elems, counts, op="sum"):
     return out.cpu().numpy()
 
 
+@pytest.mark.parametrize("length", [1, 3, 31, 32, 100])
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_reduce_cl_many_short_elements(cuda, length, op):
+    """The literal form: thousands of short elements per partition (warp-wide
+    stage-1 folds for length < 32, thread folds otherwise), elements packed
+    contiguously — bit-exact left folds + pairing tree."""
+    from paper_1505_01120_b200 import ops
+
+    count = 5000 if length < 32 else 700
+    counts = [count // 4 + (1 if p < count % 4 else 0) for p in range(4)]
+    counts[2] += counts[1]
+    counts[1] = 0  # an empty partition in the middle
+    x = (O.fill_uniform(61, count * length) * np.float32(2) - np.float32(1)).astype(np.float32)
+    elems = x.reshape(count, length)
+    xd = torch.from_numpy(x).to(cuda)
+    ptrs = torch.tensor([xd.data_ptr() + 4 * length * i for i in range(count)], dtype=torch.int64, device=cuda)
+    out = torch.empty(length, dtype=torch.float32, device=cuda)
+    ops.reduce_cl_vectors(ptrs, count, length, counts, op, out)
+    want = O.reduce_cl(elems, counts, op)
+    assert np.array_equal(_bits(out), want.view(np.uint32))
+    # integer sums, same shape
+    xi = (x.view(np.uint32).astype(np.int64) << 20) - (1 << 40)
+    xid = torch.from_numpy(xi).to(cuda)
+    ptrs_i = torch.tensor([xid.data_ptr() + 8 * length * i for i in range(count)], dtype=torch.int64, device=cuda)
+    outi = torch.empty(length, dtype=torch.int64, device=cuda)
+    ops.reduce_cl_vectors(ptrs_i, count, length, counts, "sum", outi, dtype="i64")
+    assert np.array_equal(outi.cpu().numpy(), O.reduce_cl(xi.reshape(count, length), counts))
+
+
 def test_reduce_cl_isum_golden(cuda, golden):
     from test_oracle_golden import _isum_cases
 
