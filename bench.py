@@ -115,7 +115,9 @@ def reference_arm(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(args, world=1),
+        "config": {k: v for k, v in workload_config(args, world=1).items()
+                   if k in ("workload", "elements", "partitions", "part_len")} | {
+            "path": "unmodified ucores Engine + WorkerRuntime + host executor (oracle/_ref), host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result_bits": r["result_bits"],
