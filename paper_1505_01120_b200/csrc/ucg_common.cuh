@@ -134,6 +134,6 @@ namespace ucg {
 // Work item = one aligned block of 2^item_log2 floats of one segment (the
 // last item of a segment may be partial). The size is picked per segment
 // table in [2^11, 2^14] so the last wave of warps is nearly full.
-constexpr int kMinItemLog2 = 11;
+constexpr int kMinItemLog2 = 10;  // one 1024-float chunk
 constexpr int kMaxItemLog2 = 14;
 }  // namespace ucg

@@ -197,6 +197,7 @@ constexpr int kTreeBlock = 8 * kTreeThreads;
 struct TreeSmem {
   float warp_root[kWarps];
   float stk[64];
+  float seg[32];  // single-finisher tail: the partition values
 };
 
 // Tree over n values (L2-resident item roots or partition values) by ONE CTA
@@ -265,6 +266,7 @@ struct FinishArgs {
   uint32_t epoch;
   uint32_t* err;              // set to 1 when a wait times out
   int warp_mode;              // one warp (not one CTA) per segment
+  uint32_t finishers;         // fused tail: finisher CTAs (0 = min(G, nseg))
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -324,7 +326,10 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
     for (uint64_t s = j * kWarps + (threadIdx.x >> 5); s < p.nseg; s += F * kWarps) {
       const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
       const float r = n ? warp_tree<Op>(p.partial + f, n, lane) : Op::empty();
-      if (lane == 0) __stcg(p.out + s, r);
+      if (lane == 0) {
+        __stcg(p.out + s, r);
+        if (F == 1 && s < 32) sm.seg[s] = r;
+      }
     }
     return;
   }
@@ -347,19 +352,40 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
   __shared__ bool last;
   const int tid = threadIdx.x;
   __syncthreads();
-  if (tid == 0) {
+  if (F == 1) {
+    // the only finisher wrote every partition value itself: the barrier
+    // orders those stores before the reads below, no ticket needed
+    if (tid == 0) {
+      p.done[0] = 0;
+      p.done[1] = 0;
+      p.done[2] = 0;
+    }
+  } else {
+    if (tid == 0) {
+      __threadfence();
+      last = atomicAdd(p.done + 1, 1u) == F - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    if (tid == 0) {
+      p.done[0] = 0;
+      p.done[1] = 0;
+      p.done[2] = 0;
+    }
     __threadfence();
-    last = atomicAdd(p.done + 1, 1u) == F - 1;
   }
-  __syncthreads();
-  if (!last) return;
-  if (tid == 0) {
-    p.done[0] = 0;
-    p.done[1] = 0;
-    p.done[2] = 0;
-  }
-  __threadfence();
   if (!p.result) return;
+  if (F == 1 && p.world <= 1 && p.warp_mode && p.nseg && p.nseg <= 32) {
+    // stage 2 over <= 32 values from shared memory by warp 0: the padded
+    // pairing tree is 5 xor-shuffle levels (lower lane = left operand)
+    if (tid < 32) {
+      float r = uint64_t(tid) < p.nseg ? sm.seg[tid] : Op::identity();
+#pragma unroll
+      for (int j = 0; j < 5; ++j) r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1 << j), !((tid >> j) & 1));
+      if (tid == 0) *p.result = r;
+    }
+    return;
+  }
   const float* vals = p.out;
   uint64_t nvals = p.nseg;
   if (p.world > 1) {
@@ -417,6 +443,12 @@ struct Pass1Args {
 
 template <class Op, bool kMap, int U, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const __grid_constant__ Pass1Args p) {
+  // Programmatic dependent launch (small tables, see launch_pass1): this grid
+  // may be resident before the previous step's grid has finished; wait for it
+  // (its y, partials and counter reset) before touching memory, and let the
+  // next step's grid launch now. Both are no-ops without the launch attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
@@ -446,7 +478,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   __shared__ TreeSmem sm;
   __shared__ uint32_t ticket;
   const uint32_t G = gridDim.x;
-  const uint32_t F = uint32_t(umin(G, p.fin.nseg ? p.fin.nseg : 1));
+  const uint32_t F = p.fin.finishers ? p.fin.finishers : uint32_t(umin(G, p.fin.nseg ? p.fin.nseg : 1));
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -700,10 +732,21 @@ cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_
   cfg.blockDim = dim3(kWarps * 32);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = args.finish ? 1 : 0;
+  // co-residency is needed only when several finisher CTAs wait for the
+  // whole grid; a single finisher is the last CTA out and never waits, so
+  // that launch instead overlaps its ramp with the previous step's tail
+  // (programmatic dependent launch; C1: the whole step is ~6 us)
+  static const bool no_pdl = getenv("UCG_NO_PDL") != nullptr;
+  if (args.finish && args.fin.finishers != 1) {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.numAttrs = 1;
+  } else if (!no_pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 1;
+  }
   return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, args);
 }
 
@@ -752,7 +795,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     return fail(UCG_ERR_ARG, "segment table was created on device " + std::to_string(t->device) +
                                  ", current device is " + std::to_string(dev));
   }
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr, 0};
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr, 0, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -768,6 +811,17 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
   // has only min(G, P) finisher CTAs; G = 2 CTAs per SM)
   f.warp_mode = fused_finish && t->nseg > uint64_t(sm_count()) * 4 &&
                 t->max_items_per_seg <= (uint64_t(256) << kWarpTreeDepth);
+  // small tables (C1: 4 partitions of 2^8 items): the last CTA to leave the
+  // stream runs every partition tree (one warp each) and stage 2 itself, when
+  // that is at most two rounds of one 256-value block per warp — no finisher
+  // phase, no second wait. Saves ~2 us of a ~10 us step.
+  if (fused_finish && !getenv("UCG_MULTI_FINISHER")) {
+    const uint64_t rounds = (t->nseg + kWarps - 1) / kWarps, blocks = (t->max_items_per_seg + 255) / 256;
+    if (rounds * blocks <= 2) {
+      f.warp_mode = 1;
+      f.finishers = 1;
+    }
+  }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
                    a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, f};

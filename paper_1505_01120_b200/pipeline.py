@@ -220,14 +220,20 @@ class MapReducePipeline:
                                   xg, self.result)
         return self.result
 
-    def graph_step(self) -> torch.Tensor:
-        """step() replayed from a CUDA graph captured on first use (one GPU):
-        the kernel node and its launch attributes are fixed, so a replay costs
-        one cudaGraphLaunch instead of the Python/ctypes launch path. Sharded
-        pipelines keep step(): the peer exchange advances an epoch per launch."""
+    def graph_step(self, steps: int = 1) -> torch.Tensor:
+        """`steps` consecutive step()s replayed from one CUDA graph captured on
+        first use (one GPU): the kernel nodes and their launch attributes are
+        fixed, so a replay costs one cudaGraphLaunch instead of `steps`
+        Python/ctypes launches, and consecutive small-table steps overlap
+        launch and tail (programmatic dependent launch edges). Every step
+        still runs in full: one kernel node per step. Sharded pipelines keep
+        step(): the peer exchange advances an epoch per launch."""
         if self.world > 1:
-            return self.step()
-        if getattr(self, "_graph", None) is None:
+            for _ in range(steps):
+                r = self.step()
+            return r
+        graphs = self.__dict__.setdefault("_graphs", {})
+        if steps not in graphs:
             self.step()  # warm: allocations and lazy library state outside the capture
             torch.cuda.synchronize()
             side = torch.cuda.Stream(device=self.device)
@@ -235,10 +241,11 @@ class MapReducePipeline:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(side):
                 with torch.cuda.graph(g, stream=side):
-                    self.step()
+                    for _ in range(steps):
+                        self.step()
             torch.cuda.current_stream().wait_stream(side)
-            self._graph = g
-        self._graph.replay()
+            graphs[steps] = g
+        graphs[steps].replay()
         return self.result
 
     def exchange_error(self) -> int:
