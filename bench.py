@@ -35,6 +35,26 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 # stdout carries exactly one JSON line: NCCL's banner / INFO log goes to stderr
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_JSON_OUT = None
+
+
+def _claim_stdout() -> None:
+    """Keep the real stdout for the JSON line and point fd 1 at stderr, so
+    banners printed by native libraries (the NCCL version line) cannot land
+    in front of it."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    # bench_configs imports this file as `bench`, a second module object when
+    # bench.py runs as __main__: use the stdout that __main__ claimed
+    out = _JSON_OUT or getattr(sys.modules.get("__main__"), "_JSON_OUT", None) or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 METRIC = "mapCL+reduceCL elements/sec and % HBM roofline at 1/2/4/8 B200 vs host CPU"
 UNIT = "elements/s"
@@ -122,7 +142,7 @@ def reference_arm(args, world, rank):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "result_bits": r["result_bits"],
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -405,7 +425,7 @@ def our_arm(args, world, rank, local):
             "clocks": clk.summary(),
             "result": result,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     pipe.close()
     if world > 1:
         import torch.distributed as dist
@@ -427,4 +447,5 @@ def main():
 
 
 if __name__ == "__main__":
+    _claim_stdout()
     sys.exit(main())

@@ -358,7 +358,7 @@ def run(args, world, rank, local):
                      cpu, {"workload": "1 GiB synthetic text in 64 chunks of 16 MiB, word-start flags (u8 per byte)",
                            "bytes": total, "chunks": chunks, "dtype": "u8", "word_starts_this_rank": words})
     if rank == 0 and line is not None:
-        print(json.dumps(line), flush=True)
+        B.emit(line)
     if world > 1:
         import torch.distributed as dist
 
