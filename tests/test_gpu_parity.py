@@ -369,6 +369,38 @@ def test_graph_step_matches_eager(cuda, golden):
         pipe.close()
 
 
+@pytest.mark.parametrize("lens", [[1 << 18] * 4, [100003, 65536, 1, 40000], [4096] * 40])
+def test_graph_of_steps_pdl_chain(cuda, lens):
+    """K consecutive one-kernel steps in one CUDA graph (small tables: the
+    single-finisher tail, launched with programmatic dependent launch, so
+    step k+1's grid is resident during step k's tail) reproduce the oracle
+    bits for y, the partition values and the result — every step, not just
+    the last: y is poisoned before the replay and must come back whole."""
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    for op in ("sum", "max"):
+        pipe = MapReducePipeline(lens, op=op, fused=True, plant_max=False)
+        partials = []
+        for k, n in enumerate(lens):
+            partials.append(O.tree_reduce(O.map_affine(O.fill_uniform(1000 + k, n), 2.0, 1.0), op))
+        want = O.tree_reduce(np.array(partials, np.float32), op)
+        for steps in (1, 7, 32):
+            pipe.graph_step(steps)
+            torch.cuda.synchronize()
+            pipe.y.fill_(float("nan"))
+            pipe.partials.fill_(float("nan"))
+            pipe.result.fill_(float("nan"))
+            r = pipe.graph_step(steps)
+            torch.cuda.synchronize()
+            assert O.f32_bits(r.cpu().numpy()[0]) == O.f32_bits(want), (op, steps)
+            got = pipe.partials.cpu().numpy()[:len(lens)]
+            assert np.array_equal(got.view(np.uint32), np.array(partials, np.float32).view(np.uint32))
+            for k, n in enumerate(lens):
+                y = pipe.local_output(k).cpu().numpy()
+                assert np.array_equal(y.view(np.uint32), O.map_affine(O.fill_uniform(1000 + k, n), 2.0, 1.0).view(np.uint32))
+        pipe.close()
+
+
 @pytest.mark.slow
 def test_c2_full_size(cuda):
     """C2 at the BASELINE size (2^30 fp32, 64 partitions): size-independent checks."""
