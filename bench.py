@@ -337,7 +337,6 @@ def our_arm(args, world, rank, local):
     hc1.record()
     hc1.synchronize()
     h2d_gbs = pipe.host_x.numel() * 4 / (hc0.elapsed_time(hc1) * 1e-3) / 1e9
-    e2e_gbs = h2d / (e2e_ms * 1e-3) / 1e9
     if world > 1:
         import torch.distributed as dist
 
@@ -347,6 +346,7 @@ def our_arm(args, world, rank, local):
         hb = torch.tensor([float(h2d)], dtype=torch.float64, device=dev)
         dist.all_reduce(hb, op=dist.ReduceOp.SUM)
         h2d = int(hb.item())
+    e2e_gbs = h2d / (e2e_ms * 1e-3) / 1e9  # all ranks' uploaded bytes / max-over-ranks step time
     assert r_host == result or (r_host != r_host and result != result), (r_host, result)
 
     # ---- roofline of the dominant kernel (fused map + partition reduce) --------------

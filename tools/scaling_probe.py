@@ -34,6 +34,21 @@ def step_ms(pipe, reps=30, warm=5):
     return ts[len(ts) // 2]
 
 
+def b2b_ms(pipe, reps=50):
+    """Back-to-back steps (as bench.py times them): launch gaps included,
+    launch latency hidden."""
+    for _ in range(5):
+        pipe.step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        pipe.step()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def kernel_us(pipe, reps=10):
     from torch.profiler import ProfilerActivity, profile
 
@@ -68,10 +83,11 @@ def main():
                 os.environ.pop("UCG_ITEM_LOG2", None)
             pipe = MapReducePipeline([1 << 24] * P, op=args.op, fused=True)
             ms = step_ms(pipe)
+            b2b = b2b_ms(pipe)
             k = kernel_us(pipe)
             rec = {"G": g, "elems": n, "item_log2": round(math.log2(n / pipe.segtab.scratch_floats), 2),
                    "variant": os.environ.get("UCG_PASS1_VARIANT", "0"),
-                   "step_ms": round(ms, 4), "frac_step": round(8 * n / ms / 1e6 / HBM, 4),
+                   "step_ms": round(ms, 4), "b2b_ms": round(b2b, 4), "frac_b2b": round(8 * n / b2b / 1e6 / HBM, 4), "frac_step": round(8 * n / ms / 1e6 / HBM, 4),
                    "pass1_us": round(k.get("pass1", 0), 1), "finish_us": round(k.get("finish", 0), 1),
                    "frac_pass1": round(8 * n / (k.get("pass1", 1) * 1e3) / HBM, 4)}
             print(json.dumps(rec), flush=True)
