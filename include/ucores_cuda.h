@@ -260,6 +260,17 @@ int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* flags, void*
  * fp32 accumulation in TMEM. n must be a multiple of 128. */
 int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t n, void* stream);
 
+/* Same product, fp32-faithful ("3xTF32"): A and B are split into TF32
+ * hi + lo halves (hi = round-to-nearest TF32, lo = x - hi, exact) and the
+ * tensor cores accumulate Ahi*Bhi + Ahi*Blo + Alo*Bhi in fp32 (TMEM) — the
+ * k range is cut into chunks of 256, each accumulated from zero in TMEM and
+ * added to C with an fp32 round-to-nearest add (the tensor core's own fp32
+ * accumulation truncates). Error: rms 2.7e-6 of rms(C) at any n (cuBLAS
+ * SGEMM: 0.3-1.6e-6; TF32: 7e-4), at ~a third of the TF32 rate. Finite data
+ * only: an inf operand turns into nan (inf * the zero lo half of an exact
+ * partner). Workspace 4 n^2 floats from the stream-ordered pool. */
+int ucg_gemm_f32(const float* A, const float* B, float* C, uint64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

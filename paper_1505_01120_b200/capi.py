@@ -86,6 +86,7 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_sobel_band_u8": (i32, [vp, vp, u64, u64, vp]),
     "ucg_sobel_bands_u8": (i32, [vp, P(u64), vp, P(u64), P(u64), u64, u64, vp]),
     "ucg_gemm_tf32": (i32, [vp, vp, vp, u64, vp]),
+    "ucg_gemm_f32": (i32, [vp, vp, vp, u64, vp]),
     "ucg_word_start_flags": (i32, [vp, u64, vp, vp]),
 }
 

@@ -357,9 +357,18 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
       : "memory");
 }
 
+// kTerms = 1: C = A*B in TF32 (the tensor core reads the top 19 bits of
+// each fp32 operand). kTerms = 3 (fp32-faithful "3xTF32"): the operands are
+// pre-split into x = hi + lo with hi = rna_tf32(x) and lo = x - hi (exact),
+// and the k loop runs three times over (Ahi,Bhi), (Ahi,Blo), (Alo,Bhi) into
+// the same TMEM accumulator — the dropped lo*lo term and lo's own TF32
+// truncation are ~2^-22 relative, fp32-level. tmA/tmB are then Ahi/Bhi and
+// tmA2/tmB2 Alo/Blo.
+template <int kTerms>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     k_gemm_tf32_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    float* __restrict__ C, int n) {
+                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                    float* __restrict__ C, int n, int nchunks) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[S2], empty[S2], tfull[2], tempty[2];
@@ -367,7 +376,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int tiles_m = n / 256, tiles_n = n / 256, ntiles = tiles_m * tiles_n, nk = n / BK;
+  // A work unit is (tile, k-chunk): the k range is cut into nchunks chunks,
+  // each accumulated from zero in TMEM (all kTerms terms) and added to C by
+  // the epilogue with an IEEE round-to-nearest fp32 add (C = chunk 0, then
+  // C += chunk c). The tensor core's own fp32 accumulation truncates, so its
+  // error grows linearly with the k length it accumulates; short chunks
+  // bound that. nchunks = 1: one unit per tile, C stored once.
+  const int tiles_m = n / 256, tiles_n = n / 256, ntiles = tiles_m * tiles_n, nk1 = n / BK;
+  const int kc = nk1 / nchunks;  // k-blocks per chunk (per term)
+  const int nk = kTerms * kc;    // k-blocks per unit
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S2; ++s) {
@@ -381,6 +398,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    if (kTerms > 1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA2) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB2) : "memory");
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_slot)),
@@ -405,23 +426,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           nb = idx / gm;
         }
         const int m0 = mb * 256 + int(rank) * 128, n0 = nb * 256 + int(rank) * 128;
-        for (int kb = 0; kb < nk; ++kb, ++q) {
-          const int s = int(q % S2);
-          if (q >= uint32_t(S2)) mbar_wait(&empty[s], ((q / S2) & 1) ^ 1);
-          uint8_t* a = smem + s * STAGE2_BYTES;
-          uint8_t* b = a + A2_BYTES;
-          const uint32_t lbar = smem_addr(&full[s]) & kPeerMask;
-          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
-          tma_2d_2sm(a, &tmA, lbar, kb * BK, m0);
+        for (int c = 0; c < nchunks; ++c) {
+          for (int kb = 0; kb < nk; ++kb, ++q) {
+            const int s = int(q % S2);
+            if (q >= uint32_t(S2)) mbar_wait(&empty[s], ((q / S2) & 1) ^ 1);
+            uint8_t* a = smem + s * STAGE2_BYTES;
+            uint8_t* b = a + A2_BYTES;
+            const uint32_t lbar = smem_addr(&full[s]) & kPeerMask;
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
+            // term 0: (Ahi, Bhi), 1: (Ahi, Blo), 2: (Alo, Bhi)
+            const int term = kTerms > 1 ? kb / kc : 0, k0 = (c * kc + kb - term * kc) * BK;
+            tma_2d_2sm(a, term == 2 ? &tmA2 : &tmA, lbar, k0, m0);
+            const CUtensorMap* mb_ = term == 1 ? &tmB2 : &tmB;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) tma_2d_2sm(b + j * B_STRIP, &tmB, lbar, n0 + 32 * j, kb * BK);
+            for (int j = 0; j < 4; ++j) tma_2d_2sm(b + j * B_STRIP, mb_, lbar, n0 + 32 * j, k0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       uint32_t q = 0, i = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++i) {
+      const int nunits = ((ntiles - pair + npairs - 1) / npairs) * nchunks;  // this pair's units
+      for (int u = 0; u < nunits; ++u, ++i) {
         const uint32_t acc = i & 1;
         if (i >= 2) mbar_wait(&tempty[acc], ((i / 2) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -447,7 +474,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     const int lg = warp & 3;
     const uint32_t leader_tempty[2] = {smem_addr(&tempty[0]) & kPeerMask, smem_addr(&tempty[1]) & kPeerMask};
     uint32_t i = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++i) {
+    for (int u = 0; u < ((ntiles - pair + npairs - 1) / npairs) * nchunks; ++u, ++i) {
+      const int t = pair + (u / nchunks) * npairs, chunk = u % nchunks;
       int mb, nb;
       {
         const int per_group = kGroupM * tiles_n;
@@ -474,11 +502,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
               "=r"(r[30]), "=r"(r[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float4* dst = reinterpret_cast<float4*>(crow + c * 32);
+        if constexpr (kTerms == 1) {
+          float4* dst = reinterpret_cast<float4*>(crow + c * 32);
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq)
-          __stcs(dst + qq, make_float4(__uint_as_float(r[4 * qq]), __uint_as_float(r[4 * qq + 1]),
-                                       __uint_as_float(r[4 * qq + 2]), __uint_as_float(r[4 * qq + 3])));
+          for (int qq = 0; qq < 8; ++qq)
+            __stcs(dst + qq, make_float4(__uint_as_float(r[4 * qq]), __uint_as_float(r[4 * qq + 1]),
+                                         __uint_as_float(r[4 * qq + 2]), __uint_as_float(r[4 * qq + 3])));
+        } else {
+          // k-chunk units: the warp's 32x32 block goes through shared memory
+          // (rows padded to 33 floats: conflict-free both ways) so C is read
+          // and written a row segment of 128 B per 8 lanes instead of one
+          // 16-byte piece of 32 different rows per instruction; chunk 0
+          // stores, later chunks add (round-to-nearest) to what this warp
+          // stored for the previous chunk.
+          __shared__ float stg[4][32][33];
+          float(*blk)[33] = stg[lg];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) blk[lane][j] = __uint_as_float(r[j]);
+          __syncwarp();
+          const int rq = lane >> 3, cq = (lane & 7) * 4;
+          float* base = C + size_t(mb * 256 + int(rank) * 128 + lg * 32) * n + nb * 256 + c * 32 + cq;
+          float4 o[8];
+          if (chunk > 0) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) o[it] = __ldcg(reinterpret_cast<const float4*>(base + size_t(it * 4 + rq) * n));
+          }
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int row = it * 4 + rq;
+            float4 v = make_float4(blk[row][cq], blk[row][cq + 1], blk[row][cq + 2], blk[row][cq + 3]);
+            if (chunk > 0)
+              v = make_float4(__fadd_rn(o[it].x, v.x), __fadd_rn(o[it].y, v.y), __fadd_rn(o[it].z, v.z),
+                              __fadd_rn(o[it].w, v.w));
+            float4* dst = reinterpret_cast<float4*>(base + size_t(row) * n);
+            if (chunk + 1 == nchunks) __stcs(dst, v);
+            else __stcg(dst, v);
+          }
+          __syncwarp();
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_tempty[acc]) : "memory");
@@ -488,6 +549,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   __syncthreads();
   cluster_sync_all();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// x = hi + lo: hi = x rounded to TF32 (cvt.rna), lo = x - hi (exact in fp32).
+// Non-finite x keeps lo = 0 so inf/nan propagate like the fp32 product.
+__global__ void __launch_bounds__(256) k_split_tf32(const float4* __restrict__ x, float4* __restrict__ hi,
+                                                    float4* __restrict__ lo, uint64_t n4) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = ld_stream(x + i);
+    float h[4], l[4];
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t t;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(e[k]));
+      h[k] = __uint_as_float(t);
+      l[k] = isfinite(h[k]) ? __fsub_rn(e[k], h[k]) : 0.0f;
+    }
+    st_stream(hi + i, make_float4(h[0], h[1], h[2], h[3]));
+    st_stream(lo + i, make_float4(l[0], l[1], l[2], l[3]));
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() { return tmap_encode_fn(); }
@@ -529,7 +611,8 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   if (first_on_device(attr)) {
     UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+    UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+    UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
   }
   if (variant == 0) {
     dim3 grid(unsigned(n / BN), unsigned(n / BM));
@@ -537,7 +620,7 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   } else if (variant == 2) {
     const uint64_t ntiles = (n / 256) * (n / 256);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count() / 2))) * 2;
-    k_gemm_tf32_2sm<<<grid, 192, SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, C, int(n));
+    k_gemm_tf32_2sm<1><<<grid, 192, SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, tmA, tmB, C, int(n), 1);
   } else {
     const uint64_t ntiles = (n / BM) * (n / BN);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count())));
@@ -545,4 +628,47 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   }
   UCG_LAUNCHED();
   return UCG_OK;
+}
+
+// fp32-faithful GEMM (3xTF32): split A and B into TF32 hi/lo halves
+// (workspace: 4 n^2 floats from the stream-ordered pool), then the CTA-pair
+// kernel runs its k loop over the three cross terms.
+extern "C" int ucg_gemm_f32(const float* A, const float* B, float* C, uint64_t n, void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!n) return UCG_OK;
+  if (!A || !B || !C) return fail(UCG_ERR_ARG, "null argument");
+  if (n % BN || n > (1u << 30)) return fail(UCG_ERR_ARG, "gemm: n must be a multiple of 256");
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return fail(UCG_ERR_ARG, "gemm: 16-byte alignment required");
+  cudaStream_t st = as_stream(stream);
+  const uint64_t nn = n * n;
+  float* w = nullptr;
+  UCG_CUDA(cudaMallocAsync(&w, 4 * nn * sizeof(float), st));
+  float *ahi = w, *alo = w + nn, *bhi = w + 2 * nn, *blo = w + 3 * nn;
+  const unsigned sgrid = unsigned(std::min<uint64_t>((nn / 4 + 255) / 256, uint64_t(sm_count()) * 8));
+  k_split_tf32<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(A), reinterpret_cast<float4*>(ahi),
+                                      reinterpret_cast<float4*>(alo), nn / 4);
+  UCG_LAUNCHED();
+  k_split_tf32<<<sgrid, 256, 0, st>>>(reinterpret_cast<const float4*>(B), reinterpret_cast<float4*>(bhi),
+                                      reinterpret_cast<float4*>(blo), nn / 4);
+  UCG_LAUNCHED();
+  CUtensorMap tmAh, tmAl, tmBh, tmBl;
+  int rc = make_map(&tmAh, ahi, n, n, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_map(&tmAl, alo, n, n, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_map(&tmBh, bhi, n, n, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!rc) rc = make_map(&tmBl, blo, n, n, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (!rc) {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr))
+      UCG_CUDA(cudaFuncSetAttribute(k_gemm_tf32_2sm<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+    const uint64_t ntiles = (n / 256) * (n / 256);
+    const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count() / 2))) * 2;
+    // k-chunks of 256 (UCG_GEMM_KCHUNK overrides; must divide n)
+    int kchunk = 256;
+    if (const char* e = getenv("UCG_GEMM_KCHUNK")) kchunk = atoi(e);
+    if (kchunk < BK || kchunk % BK || n % uint64_t(kchunk)) kchunk = int(n);
+    k_gemm_tf32_2sm<3><<<grid, 192, SMEM2_BYTES, st>>>(tmAh, tmBh, tmAl, tmBl, C, int(n), int(n / kchunk));
+    UCG_LAUNCHED();
+  }
+  UCG_CUDA(cudaFreeAsync(w, st));
+  return rc;
 }

@@ -47,6 +47,15 @@ const DevCache* dev_cache(int* dev_out) {
     if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return nullptr;
     g_dev[dev].sms = p.multiProcessorCount;
     g_dev[dev].major = p.major;
+    // stream-ordered workspaces (reduce_cl partials, the 3xTF32 split) stay
+    // mapped in the device's default pool between calls instead of being
+    // unmapped at every synchronize (a 1 GB re-map costs milliseconds)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
   }
   return &g_dev[dev];
 }

@@ -161,3 +161,10 @@ def gemm_tf32(A, B, Cm, n: int, stream=None):
     _require_cuda(A, B, Cm)
     call("ucg_gemm_tf32", ptr(A), ptr(B), ptr(Cm), n, stream_handle(stream))
     return Cm
+
+
+def gemm_f32(A, B, Cm, n: int, stream=None):
+    """fp32-faithful C = A @ B on the tensor cores (3xTF32 split, ucg_gemm_f32)."""
+    _require_cuda(A, B, Cm)
+    call("ucg_gemm_f32", ptr(A), ptr(B), ptr(Cm), n, stream_handle(stream))
+    return Cm

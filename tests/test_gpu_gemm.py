@@ -62,3 +62,70 @@ def test_gemm_rejects_bad_sizes(cuda):
     x = torch.zeros(100, 100, device=cuda)
     with pytest.raises(KernelPanic):
         ops.gemm_tf32(x, x, x, 100)
+    with pytest.raises(KernelPanic):
+        ops.gemm_f32(x, x, x, 100)
+
+
+@pytest.mark.parametrize("n", [256, 768, 1024, 4096])
+def test_gemm_f32_3xtf32_vs_fp64(cuda, n):
+    """fp32-level mode (3xTF32 split, k-chunks of 256 added in fp32 with
+    round-to-nearest): rms(C - C64)/rms(C64) <= 5e-6 at every n (measured
+    2.7e-6, flat in n; cuBLAS SGEMM 0.3-1.6e-6), max <= 5e-5 * rms (measured
+    <= 1.7e-5, SGEMM 2.4e-5 at 8192), and >= 100x below plain TF32."""
+    from paper_1505_01120_b200 import ops
+
+    A, B = _rand(n, 100, cuda), _rand(n, 101, cuda)
+    Cm = torch.full((n, n), float("nan"), device=cuda)
+    ops.gemm_f32(A, B, Cm, n)
+    ref = A.double() @ B.double()
+    rms_ref = float(ref.pow(2).mean().sqrt())
+    err = float((Cm.double() - ref).pow(2).mean().sqrt()) / rms_ref
+    Ct = torch.empty_like(Cm)
+    ops.gemm_tf32(A, B, Ct, n)
+    err_tf32 = float((Ct.double() - ref).pow(2).mean().sqrt()) / rms_ref
+    assert torch.isfinite(Cm).all()
+    assert err <= 5e-6, err
+    assert err * 100 <= err_tf32, (err, err_tf32)
+    assert float((Cm.double() - ref).abs().max()) <= 5e-5 * rms_ref
+
+
+def test_gemm_f32_golden_tight(cuda, golden):
+    """The golden n=24 case zero-padded to 256 in fp32-faithful mode: within
+    1e-5 (relative to rms) of the oracle's fp32 product; the padding stays 0."""
+    from paper_1505_01120_b200 import ops
+
+    g = golden["matmul"]
+    n0 = g["n"]
+    ab = (2.0 * O.fill_uniform(g["seed"], 2 * n0 * n0) - np.float32(1.0)).astype(np.float32)
+    A0, B0 = ab[: n0 * n0].reshape(n0, n0), ab[n0 * n0:].reshape(n0, n0)
+    C0 = O.matmul(A0, B0)
+    n = 256
+    A = np.zeros((n, n), np.float32)
+    B = np.zeros((n, n), np.float32)
+    A[:n0, :n0], B[:n0, :n0] = A0, B0
+    Cm = torch.empty(n, n, device=cuda)
+    ops.gemm_f32(torch.from_numpy(A).to(cuda), torch.from_numpy(B).to(cuda), Cm, n)
+    got = Cm.cpu().numpy()
+    assert np.abs(got[:n0, :n0] - C0).max() <= 1e-5 * np.sqrt((C0.astype(np.float64) ** 2).mean())
+    assert np.all(got[n0:, :] == 0) and np.all(got[:, n0:] == 0)
+
+
+def test_gemm_f32_special_values(cuda):
+    """Non-finite operands: the affected entries are non-finite (an inf
+    operand meets a zero lo half in the cross terms, so inf comes out as
+    nan — the fp32-faithful mode is for finite data; the TF32 mode keeps
+    inf), and finite entries stay exact."""
+    from paper_1505_01120_b200 import ops
+
+    n = 256
+    A = torch.zeros(n, n, device=cuda)
+    B = torch.zeros(n, n, device=cuda)
+    A[0, 0], B[0, 0] = float("inf"), 1.0
+    A[1, 1], B[1, 1] = float("nan"), 1.0
+    A[2, 2], B[2, 2] = 3.0, 0.5
+    Cm = torch.empty(n, n, device=cuda)
+    ops.gemm_f32(A, B, Cm, n)
+    c = Cm.cpu()
+    assert not torch.isfinite(c[0, 0]) and torch.isnan(c[1, 1]) and c[2, 2] == 1.5
+    ops.gemm_tf32(A, B, Cm, n)
+    assert Cm.cpu()[0, 0] == float("inf") and Cm.cpu()[2, 2] == 1.5
