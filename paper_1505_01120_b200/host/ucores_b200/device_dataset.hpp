@@ -541,7 +541,8 @@ class DeviceEngine {
       } else {  // matmul
         for (std::size_t i = 0; i < units.size(); ++i) {
           const float* a = reinterpret_cast<const float*>(ib + units[i].in_off);
-          check(ucg_gemm_tf32(a, a + mn * mn, reinterpret_cast<float*>(ob + ounits[i].in_off), mn, st));
+          check((params_.matmul_fp32 ? ucg_gemm_f32 : ucg_gemm_tf32)(
+              a, a + mn * mn, reinterpret_cast<float*>(ob + ounits[i].in_off), mn, st));
         }
       }
     }

@@ -438,15 +438,18 @@ inline DeviceOp wordcount(std::uint64_t min_device_bytes) {
   return op;
 }
 
-/// matmul: C = A.B per task on TF32 tensor cores (tolerance, not bit-exact).
-inline DeviceOp matmul_tf32(std::size_t n) {
+/// matmul: C = A.B per task on the tensor cores (tolerance, not bit-exact):
+/// fp32-faithful 3xTF32 (ucg_gemm_f32, rms error ~3e-6 of rms(C), the
+/// default: the reference kernel is fp32) or plain TF32 (ucg_gemm_tf32, 3x
+/// the rate, rms error ~7e-4).
+inline DeviceOp matmul_tc(std::size_t n, bool fp32_faithful = true) {
   DeviceOp op;
   op.arity = ucores::KernelArity::Unary;
-  auto body = [n](Gpu& g, const float* ab_host, float* c_host) {
+  auto body = [n, fp32_faithful](Gpu& g, const float* ab_host, float* c_host) {
     float* dab = static_cast<float*>(g.scratch(0).ensure(2 * n * n * 4));
     float* dc = static_cast<float*>(g.scratch(1).ensure(n * n * 4));
     g.h2d(dab, ab_host, 2 * n * n * 4);
-    check(ucg_gemm_tf32(dab, dab + n * n, dc, n, g.stream()));
+    check((fp32_faithful ? ucg_gemm_f32 : ucg_gemm_tf32)(dab, dab + n * n, dc, n, g.stream()));
     g.d2h(c_host, dc, n * n * 4);
     g.sync();
   };
@@ -476,6 +479,7 @@ struct WorkloadParams {
   float a = 2.0f, b = 1.0f;     // axpb
   std::size_t sobel_width = 16384;
   std::size_t matmul_n = 8192;
+  bool matmul_fp32 = true;  // fp32-faithful 3xTF32 (false: plain TF32)
   std::uint64_t wordcount_min_device_bytes = 65536;  // EngineConfig::min_device_bytes (engine.hpp:18)
 };
 
@@ -505,7 +509,7 @@ inline void register_workload(ucores::KernelRegistry& reg, DeviceOpRegistry& ops
   ops.add("isum2", device_ops::elementwise2_i64());
   ops.add("pi", device_ops::pi());
   ops.add("sobel", device_ops::sobel(p.sobel_width));
-  ops.add("matmul", device_ops::matmul_tf32(p.matmul_n));
+  ops.add("matmul", device_ops::matmul_tc(p.matmul_n, p.matmul_fp32));
 }
 
 }  // namespace ucores_b200
