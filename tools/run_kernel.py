@@ -20,6 +20,19 @@ elif which == "pi":
     hits = torch.empty(64, dtype=torch.int64, device="cuda")
     for _ in range(2):
         ops.pi_hits([42 + t for t in range(64)], [(1 << 30) // 64] * 64, hits)
+elif which == "gemm_f32":
+    n = 8192
+    A = torch.randn(n, n, device="cuda")
+    B = torch.randn(n, n, device="cuda")
+    C = torch.empty(n, n, device="cuda")
+    for _ in range(2):
+        ops.gemm_f32(A, B, C, n)
+elif which == "c1":
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    pipe = MapReducePipeline([1 << 18] * 4, plant_max=False)
+    for _ in range(4):
+        pipe.step()
 elif which == "gemm":
     n = 8192
     A = torch.randn(n, n, device="cuda")
