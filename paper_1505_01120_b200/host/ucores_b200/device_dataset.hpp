@@ -26,7 +26,9 @@
 #pragma once
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -182,10 +184,92 @@ class DeviceDataset {
   std::vector<std::shared_ptr<GpuAlloc>> bufs_;  // one per engine GPU (may be null)
 };
 
+/// Persistent host threads for the staging copies (a pageable Element payload
+/// into a pinned staging half): one parallel memcpy per call, split into
+/// equal slices; no thread creation on the upload path.
+class CopyPool {
+ public:
+  explicit CopyPool(unsigned n) {
+    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+    n_ = n;
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len) {
+    if (n_ <= 1 || len < (1u << 20)) {
+      std::memcpy(dst, src, len);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = dst;
+      src_ = src;
+      len_ = len;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    slice(0, dst, src, len);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void slice(unsigned i, std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len) const {
+    const std::uint64_t per = (len + n_ - 1) / n_;
+    const std::uint64_t b = std::min(len, i * per), e = std::min(len, b + per);
+    if (b < e) std::memcpy(dst + b, src + b, e - b);
+  }
+  void loop(unsigned i) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      std::uint8_t* dst;
+      const std::uint8_t* src;
+      std::uint64_t len;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        dst = dst_;
+        src = src_;
+        len = len_;
+      }
+      slice(i, dst, src, len);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  unsigned n_ = 1;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  bool stop_ = false;
+  std::uint64_t gen_ = 0;
+  unsigned pending_ = 0;
+  std::uint8_t* dst_ = nullptr;
+  const std::uint8_t* src_ = nullptr;
+  std::uint64_t len_ = 0;
+};
+
 class DeviceEngine {
  public:
   explicit DeviceEngine(WorkloadParams params = {}, int max_gpus = -1) : params_(params) {
     for (auto& g : open_gpus(max_gpus)) gpus_.push_back(std::move(g));
+    // bring-up: the upload path's pinned staging halves (2 x 64 MB per GPU)
+    // and copy threads exist before the first upload, as a worker's
+    // resources exist before its first task
+    staging_.resize(gpus_.size());
+    for (std::size_t g = 0; g < gpus_.size(); ++g) ensure_staging(g);
+    ensure_copy_pool();
   }
   std::size_t gpu_count() const { return gpus_.size(); }
 
@@ -579,15 +663,8 @@ class DeviceEngine {
       check(ucg_memcpy_h2d(dst, pieces[0].first, total, gpu.stream()));
       return;
     }
-    if (staging_.size() < gpus_.size()) staging_.resize(gpus_.size());
-    Staging& s = staging_[g];
-    if (!s.buf[0]) {
-      for (int k = 0; k < 2; ++k) {
-        check(ucg_host_alloc(&s.buf[k], kStageBytes));
-        check(ucg_event_create(&s.ev[k]));
-      }
-    }
-    const unsigned threads = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    Staging& s = ensure_staging(g);
+    ensure_copy_pool();
     std::uint8_t* stage = nullptr;
     std::uint64_t fill = 0, dev_off = 0;
     int k = 0;
@@ -611,24 +688,33 @@ class DeviceEngine {
       for (std::uint64_t off = 0; off < n;) {
         if (!stage) acquire();
         const std::uint64_t len = std::min(kStageBytes - fill, n - off);
-        if (len >= (1u << 20) && threads > 1) {  // large piece: parallel host copy
-          const std::uint64_t per = (len + threads - 1) / threads;
-          std::vector<std::thread> pool;
-          for (unsigned t = 1; t < threads; ++t) {
-            const std::uint64_t b = std::min(len, t * per), e = std::min(len, b + per);
-            if (b < e) pool.emplace_back([=] { std::memcpy(stage + fill + b, src + off + b, e - b); });
-          }
-          std::memcpy(stage + fill, src + off, std::min(len, per));
-          for (auto& th : pool) th.join();
-        } else {
-          std::memcpy(stage + fill, src + off, len);
-        }
+        copy_pool_->copy(stage + fill, src + off, len);  // all host threads for large pieces
         fill += len;
         off += len;
         if (fill == kStageBytes) flush();
       }
     }
     flush();
+  }
+
+  Staging& ensure_staging(std::size_t g) {
+    if (staging_.size() < gpus_.size()) staging_.resize(gpus_.size());
+    Staging& s = staging_[g];
+    if (!s.buf[0]) {
+      DeviceGuard guard;
+      gpus_[g]->bind();
+      for (int k = 0; k < 2; ++k) {
+        check(ucg_host_alloc(&s.buf[k], kStageBytes));
+        check(ucg_event_create(&s.ev[k]));
+      }
+    }
+    return s;
+  }
+  void ensure_copy_pool() {
+    if (copy_pool_) return;
+    unsigned n = std::max(1u, std::thread::hardware_concurrency());
+    if (const char* e = std::getenv("UCG_COPY_THREADS")) n = std::max(1, std::atoi(e));  // A/B runs
+    copy_pool_ = std::make_unique<CopyPool>(n);
   }
 
   // -- helpers ----------------------------------------------------------------------
@@ -719,6 +805,7 @@ class DeviceEngine {
   std::shared_ptr<DevicePool> pool_ = std::make_shared<DevicePool>();
   std::vector<std::pair<std::string, std::unique_ptr<ucg_segtab, TabFree>>> tabs_;
   std::vector<Staging> staging_;
+  std::unique_ptr<CopyPool> copy_pool_;
 };
 
 }  // namespace ucores_b200
