@@ -192,7 +192,9 @@ __device__ __forceinline__ float work_item(const float* __restrict__ x, float* _
 // ---- trees over values in global memory ----------------------------------------
 
 constexpr int kTreeThreads = 256;  // == kWarps * 32: pass 1 CTAs run the trees too
-constexpr int kTreeBlock = 8 * kTreeThreads;
+constexpr int kTreeVals = 16;  // values per thread per block: 4096-value blocks (one
+                               // per C2 partition of 2^24 floats in 2^12-float items)
+constexpr int kTreeBlock = kTreeVals * kTreeThreads;
 
 struct TreeSmem {
   float warp_root[kWarps];
@@ -202,8 +204,9 @@ struct TreeSmem {
 
 // Tree over n values (L2-resident item roots or partition values) by ONE CTA
 // of 256 threads, padded to a power of two with the identity. Values are
-// consumed in aligned blocks of 2048: thread t combines its 8 contiguous
-// values (3 tree levels in registers), the warp finishes 5 levels with xor
+// consumed in aligned blocks of 4096: thread t combines its 16 contiguous
+// values (4 tree levels in registers, all 16 loads in flight at once), the
+// warp finishes 5 levels with xor
 // shuffles (lower lane = left operand), thread 0 the last 3 over the warp
 // roots — one barrier per block. Block roots are merged by a binary-counter
 // stack of aligned subtrees and the stack is folded right to left.
@@ -212,12 +215,29 @@ __device__ float cta_tree(const float* __restrict__ vals, uint64_t n, TreeSmem& 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint64_t nblocks = (n + kTreeBlock - 1) / kTreeBlock;
   for (uint64_t bi = 0; bi < nblocks; ++bi) {
-    const uint64_t base = bi * kTreeBlock + 8 * uint64_t(tid);
-    float v[8];
+    const uint64_t base = bi * kTreeBlock + kTreeVals * uint64_t(tid);
+    float v[kTreeVals];
+    if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(vals + base) & 15) == 0) {
+      // 4 x 16-byte loads (a quarter of the L2 sector requests of scalar loads)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = base + k < n ? __ldcg(vals + base + k) : Op::identity();
-    float r = Op::apply(Op::apply(Op::apply(v[0], v[1]), Op::apply(v[2], v[3])),
-                        Op::apply(Op::apply(v[4], v[5]), Op::apply(v[6], v[7])));
+      for (int k = 0; k < kTreeVals / 4; ++k) {
+        const float4 q = __ldcg(reinterpret_cast<const float4*>(vals + base) + k);
+        v[4 * k] = q.x;
+        v[4 * k + 1] = q.y;
+        v[4 * k + 2] = q.z;
+        v[4 * k + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kTreeVals; ++k) v[k] = base + k < n ? __ldcg(vals + base + k) : Op::identity();
+    }
+    // balanced pairwise tree over the thread's aligned 16 values
+#pragma unroll
+    for (int w = kTreeVals / 2; w >= 1; w /= 2) {
+#pragma unroll
+      for (int k = 0; k < w; ++k) v[k] = Op::apply(v[2 * k], v[2 * k + 1]);
+    }
+    float r = v[0];
 #pragma unroll
     for (int j = 0; j < 5; ++j) r = lr<Op>(r, __shfl_xor_sync(kFull, r, 1 << j), !((lane >> j) & 1));
     if (lane == 0) sm.warp_root[w] = r;
