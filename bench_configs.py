@@ -132,14 +132,17 @@ def run(args, world, rank, local):
         total = torch.empty(1, dtype=torch.int64, device=dev)
         total_host = torch.empty(1, dtype=torch.int64).pin_memory()
 
+        xg = None
+        if world > 1:
+            from paper_1505_01120_b200.pipeline import open_exchange
+
+            xg = open_exchange(world, rank, 2, 2 * rank, 2 * world)
+
         def fn():
             # map_cl(pi) over this rank's tasks + reduce_cl(isum2) in one launch;
-            # sharded: one int64 all-reduce (NCCL) combines the rank totals
-            ops.pi_hits(seeds, samples, hits, total_out=total)
-            if world > 1:
-                import torch.distributed as dist
-
-                dist.all_reduce(total)
+            # sharded: the same launch's last CTA exchanges the rank totals over
+            # NVLink (P2P stores + epoch flags), so every rank ends with the sum
+            ops.pi_hits(seeds, samples, hits, total_out=total, xchg=xg)
         fn()
         with B.ClockSampler(local) as clk:
             l0 = capi.launch_count()
@@ -155,6 +158,12 @@ def run(args, world, rank, local):
         fn()
         total_hits = int(total.item())
         assert total_hits == int(hits.sum().item()) or world > 1
+        if world > 1:  # the fused exchange's sum equals an NCCL all-reduce of the rank totals
+            import torch.distributed as dist
+
+            chk = hits.sum().reshape(1).clone()
+            dist.all_reduce(chk)
+            assert int(chk.item()) == total_hits, (int(chk.item()), total_hits)
         if rank == 0 and world == 1:
             r = _ref_workload(["--w", "pi", "--samples", str(1 << 28), "--tasks", "64", "--steps", "1", "--warmup", "0"])
             cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "samples/s", "cores": r["threads"],
@@ -169,7 +178,7 @@ def run(args, world, rank, local):
                       "frac": achieved / ipc_peak, "traffic": 0, "note": "integer-ALU / issue bound; no HBM traffic"},
                      cpu, {"workload": CONFIGS[2], "samples": S, "tasks": T, "dtype": "u64/f64->i64",
                            "hits_total": total_hits,
-                           "exchange": "none" if world == 1 else "one int64 NCCL all-reduce of the rank totals"})
+                           "exchange": "none" if world == 1 else "rank totals exchanged inside the counting kernel over NVLink (P2P stores + epoch flags)"})
     elif args.workload == "c4":
         H = W = 16384
         R = 256

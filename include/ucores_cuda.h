@@ -192,6 +192,16 @@ int ucg_xchg_destroy(ucg_xchg* x);
 int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, float a, float b, int op,
                               float* scratch, float* partials, ucg_xchg* xchg, float* result, void* stream);
 
+/* Sharded map_cl(pi) + reduce_cl(isum2) (C3 over GPUs, one process per
+ * GPU): ucg_pi_hits_total over this rank's tasks, and the last CTA of the
+ * launch exchanges the rank totals over NVLink (8-byte P2P stores into every
+ * peer's region + epoch flags, as ucg_segment_reduce_cl_f32) so *total_out
+ * ends as the sum over ALL ranks — no collective call. xchg: created with
+ * nloc = 2, part_offset = 2*rank, p_total = 2*world, opened. A rank with no
+ * tasks still joins the exchange. */
+int ucg_pi_hits_total_xchg(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,
+                           int64_t* total_out, ucg_xchg* xchg, void* stream);
+
 /* reduceCL stage 2 over n one-float partials in partition order: the pairing
  * tree with odd promotion (engine.hpp:172-190). out: one float (device). */
 int ucg_tree_reduce_f32(const float* x, uint64_t n, int op, float* out, void* stream);

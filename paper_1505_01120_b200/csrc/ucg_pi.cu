@@ -59,9 +59,72 @@ __device__ __forceinline__ uint32_t pi_hit(uint64_t s0) {
   return __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)) <= 18446744073709551616.0 ? 1u : 0u;
 }
 
+// Sharded reduce_cl(isum2) over ranks, fused into the counting kernel: the
+// last CTA of the launch (exit ticket) stores this rank's total into every
+// peer's IPC-mapped region (8 bytes at slot `rank`), publishes an epoch flag
+// there (release, system scope), waits for all ranks' flags in its own
+// region (acquire) and writes the sum over ranks to `total` — the same
+// NVLink exchange as the C2 reduction's tail (ucg_reduce.cu stage2).
+struct PiXchg {
+  const uint64_t* peers;   // [world] region base addresses (own at [rank]); null: no exchange
+  uint64_t flags_offset;
+  uint32_t epoch;
+  int world, rank;
+  uint32_t* err;
+  unsigned long long* done;  // exit tickets, zeroed before the launch
+};
+
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void pi_exchange(const PiXchg& x, unsigned long long* total) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // this CTA's atomics on `total` before its ticket
+    last = atomicAdd(x.done, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  __threadfence();
+  const unsigned long long mine = atomicAdd(total, 0ull);  // every CTA's hits are in
+  for (int r = lane; r < x.world; r += 32)
+    reinterpret_cast<unsigned long long*>(x.peers[r])[x.rank] = mine;
+  __threadfence_system();
+  __syncwarp();
+  for (int r = lane; r < x.world; r += 32) {
+    st_release_sys_u32(reinterpret_cast<uint32_t*>(x.peers[r] + x.flags_offset) + x.rank, x.epoch);
+  }
+  const uint32_t* flags = reinterpret_cast<const uint32_t*>(x.peers[x.rank] + x.flags_offset);
+  for (int r = lane; r < x.world; r += 32) {
+    uint64_t spins = 0;
+    while (int32_t(ld_acquire_sys_u32(flags + r) - x.epoch) < 0) {
+      __nanosleep(64);
+      if (++spins > (1ull << 24)) {  // ~1 s: a peer never arrived
+        atomicExch(x.err, 1u);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const volatile unsigned long long* slots = reinterpret_cast<const unsigned long long*>(x.peers[x.rank]);
+    unsigned long long sum = 0;
+    for (int r = 0; r < x.world; ++r) sum += slots[r];  // exact in any order
+    *total = sum;
+  }
+}
+
 __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTasks tasks, uint64_t nunits,
                                                    unsigned long long* __restrict__ hits,
-                                                   unsigned long long* __restrict__ total) {
+                                                   unsigned long long* __restrict__ total, const PiXchg xg) {
   __shared__ uint32_t warp_sum[kPiThreads / 32];
   for (uint64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
     // task owning this unit: binary search over first_unit
@@ -101,6 +164,7 @@ __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTas
     }
     __syncthreads();
   }
+  if (xg.peers && total) pi_exchange(xg, total);
 }
 
 // Class-D form of the same body (the seam-B contract of the pi kernel):
@@ -126,14 +190,28 @@ extern "C" int ucg_pi_flags(uint64_t seed, uint64_t samples, uint8_t* flags, voi
   return UCG_OK;
 }
 
-extern "C" int ucg_pi_hits_total(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks,
-                                 int64_t* hits_out, int64_t* total_out, void* stream) {
+namespace {
+int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out, int64_t* total_out,
+              ucg_xchg* xg, void* stream) {
   if (int rc = check_device()) return rc;
   cudaStream_t st = as_stream(stream);
+  PiXchg xa{};
+  if (xg) {
+    if (!total_out) return fail(UCG_ERR_ARG, "the sharded pi total needs total_out");
+    if (!xg->opened) return fail(UCG_ERR_ARG, "exchange context not opened");
+    if (xg->p_total < 2ull * uint64_t(xg->world)) return fail(UCG_ERR_ARG, "pi exchange needs 2 slots per rank");
+    int dev = -1;
+    UCG_CUDA(cudaGetDevice(&dev));
+    if (dev != xg->device) return fail(UCG_ERR_ARG, "exchange context belongs to another device");
+    unsigned long long* done = claim_counter();
+    if (!done) return fail(UCG_ERR_CUDA, "claim counter allocation failed");
+    UCG_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned long long), st));
+    xa = PiXchg{xg->d_peers, xg->flags_offset, ++xg->epoch, xg->world, xg->rank, xg->d_err, done};
+  }
   if (total_out) UCG_CUDA(cudaMemsetAsync(total_out, 0, sizeof(int64_t), st));
-  if (!ntasks) return UCG_OK;
-  if (!seeds || !samples || !hits_out) return fail(UCG_ERR_ARG, "null argument");
-  UCG_CUDA(cudaMemsetAsync(hits_out, 0, ntasks * sizeof(int64_t), st));
+  if (ntasks && (!seeds || !samples || !hits_out)) return fail(UCG_ERR_ARG, "null argument");
+  if (ntasks) UCG_CUDA(cudaMemsetAsync(hits_out, 0, ntasks * sizeof(int64_t), st));
+  bool exchanged = false;
   for (uint64_t t0 = 0; t0 < ntasks; t0 += kMaxTasks) {
     const uint32_t nt = uint32_t(std::min<uint64_t>(kMaxTasks, ntasks - t0));
     PiTasks p;
@@ -147,11 +225,36 @@ extern "C" int ucg_pi_hits_total(const uint64_t* seeds, const uint64_t* samples,
     const uint64_t nunits = p.first_unit[nt];
     if (!nunits) continue;
     const unsigned grid = unsigned(std::min<uint64_t>(nunits, uint64_t(sm_count()) * 8));
+    // the exchange rides on the last launch (earlier chunks' hits are in
+    // `total` by stream order)
+    const bool last_chunk = t0 + kMaxTasks >= ntasks;
+    const PiXchg xl = last_chunk ? xa : PiXchg{};
+    exchanged |= last_chunk && xa.peers;
     k_pi<<<grid, kPiThreads, 0, st>>>(p, nunits, reinterpret_cast<unsigned long long*>(hits_out + t0),
-                                      reinterpret_cast<unsigned long long*>(total_out));
+                                      reinterpret_cast<unsigned long long*>(total_out), xl);
+    UCG_LAUNCHED();
+  }
+  if (xa.peers && !exchanged) {
+    // no samples on this rank (or none in its last chunk): it still joins
+    // the exchange, with its total as it stands
+    PiTasks p;
+    p.ntasks = 0;
+    p.first_unit[0] = 0;
+    k_pi<<<1, kPiThreads, 0, st>>>(p, 0, nullptr, reinterpret_cast<unsigned long long*>(total_out), xa);
     UCG_LAUNCHED();
   }
   return UCG_OK;
+}
+}  // namespace
+
+extern "C" int ucg_pi_hits_total(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks,
+                                 int64_t* hits_out, int64_t* total_out, void* stream) {
+  return pi_launch(seeds, samples, ntasks, hits_out, total_out, nullptr, stream);
+}
+
+extern "C" int ucg_pi_hits_total_xchg(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks,
+                                      int64_t* hits_out, int64_t* total_out, ucg_xchg* xg, void* stream) {
+  return pi_launch(seeds, samples, ntasks, hits_out, total_out, xg, stream);
 }
 
 extern "C" int ucg_pi_hits(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out,

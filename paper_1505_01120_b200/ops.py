@@ -128,11 +128,18 @@ def reduce_cl_vectors(elem_ptrs, count: int, length: int, part_counts: Sequence[
     return out
 
 
-def pi_hits(seeds: Sequence[int], samples: Sequence[int], hits_out, stream=None, total_out=None):
+def pi_hits(seeds: Sequence[int], samples: Sequence[int], hits_out, stream=None, total_out=None, xchg=None):
     """Monte-Carlo pi mapCL over tasks {seed, samples}; with
-    total_out, also the reduce_cl(isum2) of the task hits, in the same launch."""
+    total_out, also the reduce_cl(isum2) of the task hits, in the same launch;
+    with xchg (an opened exchange context, pipeline.open_exchange with 2 slots
+    per rank), total_out is the sum over all ranks, exchanged over NVLink by
+    the same kernel."""
     _require_cuda(hits_out)
-    if total_out is None:
+    if xchg is not None:
+        _require_cuda(total_out)
+        call("ucg_pi_hits_total_xchg", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out),
+             ptr(total_out), xchg, stream_handle(stream))
+    elif total_out is None:
         call("ucg_pi_hits", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out), stream_handle(stream))
     else:
         _require_cuda(total_out)

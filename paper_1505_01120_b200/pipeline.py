@@ -101,6 +101,27 @@ class Layout:
         return cls(list(lens), begins, max(off, align))
 
 
+def open_exchange(world: int, rank: int, nloc: int, part_offset: int, p_total: int, group=None) -> int:
+    """A peer-exchange context (include/ucores_cuda.h ucg_xchg_*): this rank's
+    IPC-exported region, every rank's handle all-gathered once through
+    torch.distributed (the only host-side collective; the per-step exchange
+    runs inside the kernels over NVLink) and opened. Returns the handle."""
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    h = C.c_void_p()
+    capi.call("ucg_xchg_create", world, rank, nloc, part_offset, p_total, C.byref(h), phase="map_parameters")
+    nbytes = int(capi.load().ucg_xchg_handle_bytes())
+    mine = (C.c_char * nbytes)()
+    capi.call("ucg_xchg_export", h.value, mine)
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(mine), group=group)
+    allh = (C.c_char * (nbytes * world)).from_buffer_copy(b"".join(handles))
+    capi.call("ucg_xchg_open", h.value, allh)
+    return h.value
+
+
 class MapReducePipeline:
     """One rank's share of the C1/C2 pipeline, inputs resident in HBM."""
 
@@ -187,21 +208,7 @@ class MapReducePipeline:
         return self.result
 
     def _setup_xchg(self) -> None:
-        import ctypes as C
-
-        import torch.distributed as dist
-
-        h = C.c_void_p()
-        capi.call("ucg_xchg_create", self.world, self.rank, len(self.local_lens), self.owned.start, self.P,
-                  C.byref(h), phase="map_parameters")
-        self.xchg = h.value
-        nbytes = int(capi.load().ucg_xchg_handle_bytes())
-        mine = (C.c_char * nbytes)()
-        capi.call("ucg_xchg_export", self.xchg, mine)
-        handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(mine), group=self.group)
-        allh = (C.c_char * (nbytes * self.world)).from_buffer_copy(b"".join(handles))
-        capi.call("ucg_xchg_open", self.xchg, allh)
+        self.xchg = open_exchange(self.world, self.rank, len(self.local_lens), self.owned.start, self.P, self.group)
 
     def step(self) -> torch.Tensor:
         """One pass: map + partition reduce + reduce_cl (+ exchange when sharded)."""

@@ -37,6 +37,26 @@ def main():
         report["cases"].append({"P": P, "op": op, "exchange": exchange, "ok": ok, "got": r, "want": float(want)})
         report["ok"] &= ok
         pipe.close()
+    # C3 sharded: map_cl(pi) + reduce_cl(isum2), the rank totals exchanged
+    # inside the counting kernel over NVLink; T = world - 1 leaves one rank
+    # without tasks (it still joins the exchange)
+    from paper_1505_01120_b200 import ops
+    from paper_1505_01120_b200.pipeline import open_exchange, shard_range
+
+    xg = open_exchange(world, rank, 2, 2 * rank, 2 * world)
+    for T, S in [(13, 300001), (max(1, world - 1), 70000)]:
+        mine = list(shard_range(T, world, rank))
+        seeds = [42 + t for t in mine]
+        samples = [S + 1000 * t for t in mine]
+        hits = torch.zeros(max(1, len(mine)), dtype=torch.int64, device="cuda")
+        total = torch.empty(1, dtype=torch.int64, device="cuda")
+        for _ in range(3):  # repeated launches exercise the epoch flags
+            ops.pi_hits(seeds, samples, hits, total_out=total, xchg=xg)
+        want = sum(O.pi_hits(42 + t, S + 1000 * t) for t in range(T))
+        got = int(total.item())
+        ok = got == want and hits.cpu().tolist()[:len(mine)] == [O.pi_hits(42 + t, S + 1000 * t) for t in mine]
+        report["cases"].append({"pi_tasks": T, "ok": ok, "got": got, "want": want})
+        report["ok"] &= ok
     print("MULTIGPU " + json.dumps(report), flush=True)
     dist.destroy_process_group()
     return 0 if report["ok"] else 1
