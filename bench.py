@@ -76,6 +76,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-engine-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the K timed steps one by one")
     ap.add_argument("--workload", default="c2", choices=["c1", "c1lit", "c2", "c3", "c4", "c5", "wc"],
                     help="c2 (default) is the headline; the others are the remaining BASELINE configs")
     ap.add_argument("--cpu-sample-parts", type=int, default=4)
@@ -216,6 +217,8 @@ def workload_config(args, world: int) -> dict:
         "steps_per_launch": ("1 kernel launch per step" if not args.no_fuse
                              else "2 kernel launches per step (map, then reduce + trees)"),
         "l2": f"inputs larger than L2 ({n * 4 // world / 2**30:.2f} GiB x per GPU)",
+        "timed_launch": ("the K steps launched one by one" if getattr(args, "no_graph", False)
+                         else "the K steps replayed from one CUDA graph of K one-kernel steps"),
     }
 
 
@@ -274,14 +277,22 @@ def our_arm(args, world, rank, local):
                 pipe.step()
             torch.cuda.synchronize()
         launches0 = capi.launch_count()
+        if not args.no_graph:
+            pipe.graph_step(k)  # capture the K-step graph (+ one warm replay), outside the timed region
         barrier()
-        # timed region 1 (value): exactly K full steps, device time
+        # timed region 1 (value): exactly K full steps, device time — replayed
+        # from one CUDA graph of K one-kernel steps (the sharded exchange's
+        # epoch advances on the device), or launched one by one (--no-graph)
         t0.record()
-        for i in range(k):
-            pipe.step()
+        if args.no_graph:
+            for i in range(k):
+                pipe.step()
+        else:
+            pipe.graph_step(k)
         t1.record()
         barrier()
-        launches = capi.launch_count() - launches0
+        # graph replays bypass the C launch counter: one k_segment_pass1 node per step
+        launches = k if not args.no_graph else capi.launch_count() - launches0
         result = float(pipe.result.item())
         # timed region 2 (roofline): K launches of the dominant kernel (the
         # fused map + partition reduce, trees in its tail), one event pair each

@@ -97,6 +97,17 @@ struct OpMax {
 };
 
 // streaming 128-bit global accesses (data is touched exactly once)
+// Peer waits give up (and raise the exchange's error flag) after this long:
+// generous, so a rank that is late to its first step (lazy module loading,
+// graph capture, host-side set-up) is waited for, while a dead peer still
+// surfaces as an error instead of a hang.
+constexpr uint64_t kPeerWaitNs = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 
@@ -122,11 +133,14 @@ struct ucg_xchg {
   int world, rank;
   uint64_t nloc, part_offset, p_total;
   uint64_t region_bytes, flags_offset;
-  uint8_t* region;          // this rank's IPC-exported buffer: [p_total floats | flags[world]]
+  uint8_t* region;          // this rank's IPC-exported buffer: [2 x p_total floats | flags[world]]
+                            // (value buffer by epoch parity: a rank one step ahead never
+                            // overwrites values a peer may still be reading)
   uint64_t* d_peers;        // [world] device addresses of every rank's region (mapped)
   uint8_t** peer_ptrs;      // host copy (opened IPC handles, own region at [rank])
   uint32_t* d_err;
-  uint32_t epoch;
+  uint32_t* d_epoch;        // exchanges completed by this rank (advanced on the device, so
+                            // sharded steps can be replayed from CUDA graphs)
   bool opened;
 };
 

@@ -68,7 +68,7 @@ __device__ __forceinline__ uint32_t pi_hit(uint64_t s0) {
 struct PiXchg {
   const uint64_t* peers;   // [world] region base addresses (own at [rank]); null: no exchange
   uint64_t flags_offset;
-  uint32_t epoch;
+  uint32_t* epoch;         // exchanges completed (device counter, advanced here)
   int world, rank;
   uint32_t* err;
   unsigned long long* done;  // exit tickets, zeroed before the launch
@@ -95,19 +95,21 @@ __device__ void pi_exchange(const PiXchg& x, unsigned long long* total) {
   const int lane = threadIdx.x;
   __threadfence();
   const unsigned long long mine = atomicAdd(total, 0ull);  // every CTA's hits are in
+  const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(x.epoch) + 1;
+  const int buf = int(epoch & 1) * x.world;  // value buffer by epoch parity
   for (int r = lane; r < x.world; r += 32)
-    reinterpret_cast<unsigned long long*>(x.peers[r])[x.rank] = mine;
+    reinterpret_cast<unsigned long long*>(x.peers[r])[buf + x.rank] = mine;
   __threadfence_system();
   __syncwarp();
   for (int r = lane; r < x.world; r += 32) {
-    st_release_sys_u32(reinterpret_cast<uint32_t*>(x.peers[r] + x.flags_offset) + x.rank, x.epoch);
+    st_release_sys_u32(reinterpret_cast<uint32_t*>(x.peers[r] + x.flags_offset) + x.rank, epoch);
   }
   const uint32_t* flags = reinterpret_cast<const uint32_t*>(x.peers[x.rank] + x.flags_offset);
   for (int r = lane; r < x.world; r += 32) {
-    uint64_t spins = 0;
-    while (int32_t(ld_acquire_sys_u32(flags + r) - x.epoch) < 0) {
+    const uint64_t t0 = global_ns();
+    while (int32_t(ld_acquire_sys_u32(flags + r) - epoch) < 0) {
       __nanosleep(64);
-      if (++spins > (1ull << 24)) {  // ~1 s: a peer never arrived
+      if (global_ns() - t0 > kPeerWaitNs) {  // a peer never arrived
         atomicExch(x.err, 1u);
         break;
       }
@@ -117,8 +119,9 @@ __device__ void pi_exchange(const PiXchg& x, unsigned long long* total) {
   if (lane == 0) {
     const volatile unsigned long long* slots = reinterpret_cast<const unsigned long long*>(x.peers[x.rank]);
     unsigned long long sum = 0;
-    for (int r = 0; r < x.world; ++r) sum += slots[r];  // exact in any order
+    for (int r = 0; r < x.world; ++r) sum += slots[buf + r];  // exact in any order
     *total = sum;
+    *x.epoch = epoch;
   }
 }
 
@@ -206,7 +209,7 @@ int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, i
     unsigned long long* done = claim_counter();
     if (!done) return fail(UCG_ERR_CUDA, "claim counter allocation failed");
     UCG_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned long long), st));
-    xa = PiXchg{xg->d_peers, xg->flags_offset, ++xg->epoch, xg->world, xg->rank, xg->d_err, done};
+    xa = PiXchg{xg->d_peers, xg->flags_offset, xg->d_epoch, xg->world, xg->rank, xg->d_err, done};
   }
   if (total_out) UCG_CUDA(cudaMemsetAsync(total_out, 0, sizeof(int64_t), st));
   if (ntasks && (!seeds || !samples || !hits_out)) return fail(UCG_ERR_ARG, "null argument");

@@ -283,7 +283,7 @@ struct FinishArgs {
   uint64_t p_total;           // P over all ranks
   const uint64_t* peers;      // [world] region base addresses (this rank's own at [rank])
   uint64_t flags_offset;      // byte offset of the [world] epoch flags inside a region
-  uint32_t epoch;
+  uint32_t* epoch;            // [1] exchanges completed (device counter; this one advances it)
   uint32_t* err;              // set to 1 when a wait times out
   int warp_mode;              // one warp (not one CTA) per segment
   uint32_t finishers;         // fused tail: finisher CTAs (0 = min(G, nseg))
@@ -408,32 +408,39 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
   }
   const float* vals = p.out;
   uint64_t nvals = p.nseg;
+  uint32_t epoch = 0;
   if (p.world > 1) {
+    // this exchange's epoch and value buffer (by parity)
+    epoch = *reinterpret_cast<volatile uint32_t*>(p.epoch) + 1;
+    const uint64_t buf = (epoch & 1) * p.p_total;
     for (int r = 0; r < p.world; ++r) {
-      float* g = reinterpret_cast<float*>(p.peers[r]) + p.part_offset;
+      float* g = reinterpret_cast<float*>(p.peers[r]) + buf + p.part_offset;
       for (uint64_t i = tid; i < p.nseg; i += blockDim.x) g[i] = __ldcg(p.out + i);
     }
     __threadfence_system();
     __syncthreads();
     if (tid < p.world) {
       uint32_t* fl = reinterpret_cast<uint32_t*>(p.peers[tid] + p.flags_offset);
-      st_release_sys(fl + p.rank, p.epoch);
+      st_release_sys(fl + p.rank, epoch);
       const uint32_t* mine = reinterpret_cast<const uint32_t*>(p.peers[p.rank] + p.flags_offset) + tid;
-      uint64_t spins = 0;
-      while (int32_t(ld_acquire_sys(mine) - p.epoch) < 0) {
+      const uint64_t t0 = global_ns();
+      while (int32_t(ld_acquire_sys(mine) - epoch) < 0) {
         __nanosleep(64);
-        if (++spins > (1ull << 24)) {  // ~1 s: a peer never arrived
+        if (global_ns() - t0 > kPeerWaitNs) {  // a peer never arrived
           atomicExch(p.err, 1u);
           break;
         }
       }
     }
     __syncthreads();
-    vals = reinterpret_cast<const float*>(p.peers[p.rank]);
+    vals = reinterpret_cast<const float*>(p.peers[p.rank]) + buf;
     nvals = p.p_total;
   }
   const float root = nvals ? cta_tree<Op>(vals, nvals, sm) : Op::empty();
-  if (tid == 0) *p.result = root;
+  if (tid == 0) {
+    *p.result = root;
+    if (p.world > 1) *p.epoch = epoch;
+  }
 }
 
 // Pass 1: one warp per work item (grid-stride over items); item roots go to
@@ -815,7 +822,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     return fail(UCG_ERR_ARG, "segment table was created on device " + std::to_string(t->device) +
                                  ", current device is " + std::to_string(dev));
   }
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, 0, nullptr, 0, 0};
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -823,7 +830,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.p_total = xg->p_total;
     f.peers = xg->d_peers;
     f.flags_offset = xg->flags_offset;
-    f.epoch = ++xg->epoch;
+    f.epoch = xg->d_epoch;
     f.err = xg->d_err;
   }
   const bool fused_finish = t->nitems && !separate_finish();

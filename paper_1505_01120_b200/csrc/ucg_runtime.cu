@@ -389,13 +389,13 @@ int ucg_xchg_create(int world, int rank, uint64_t nloc, uint64_t part_offset, ui
   x->nloc = nloc;
   x->part_offset = part_offset;
   x->p_total = p_total;
-  x->flags_offset = (p_total * 4 + 255) / 256 * 256;
+  x->flags_offset = (2 * p_total * 4 + 255) / 256 * 256;
   x->region_bytes = x->flags_offset + 256;
   x->peer_ptrs = new uint8_t*[world]();
   cudaError_t e;
   if ((e = cudaMalloc(&x->region, x->region_bytes)) != cudaSuccess || (e = cudaMemset(x->region, 0, x->region_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&x->d_peers, world * 8)) != cudaSuccess || (e = cudaMalloc(&x->d_err, 4)) != cudaSuccess ||
-      (e = cudaMemset(x->d_err, 0, 4)) != cudaSuccess) {
+      (e = cudaMalloc(&x->d_peers, world * 8)) != cudaSuccess || (e = cudaMalloc(&x->d_err, 8)) != cudaSuccess ||
+      (e = cudaMemset(x->d_err, 0, 8)) != cudaSuccess) {
     cudaFree(x->region);
     cudaFree(x->d_peers);
     cudaFree(x->d_err);
@@ -403,6 +403,7 @@ int ucg_xchg_create(int world, int rank, uint64_t nloc, uint64_t part_offset, ui
     delete x;
     return cuda_fail(e, "ucg_xchg_create");
   }
+  x->d_epoch = x->d_err + 1;  // the second word of the 8-byte allocation
   *out = x;
   return UCG_OK;
 }

@@ -233,9 +233,10 @@ class MapReducePipeline:
         fixed, so a replay costs one cudaGraphLaunch instead of `steps`
         Python/ctypes launches, and consecutive small-table steps overlap
         launch and tail (programmatic dependent launch edges). Every step
-        still runs in full: one kernel node per step. Sharded pipelines keep
-        step(): the peer exchange advances an epoch per launch."""
-        if self.world > 1:
+        still runs in full: one kernel node per step. Sharded pipelines with
+        the fused NVLink exchange replay too (its epoch advances on the
+        device, once per exchange); every rank must replay the same count."""
+        if self.world > 1 and self.exchange == "nccl":
             for _ in range(steps):
                 r = self.step()
             return r

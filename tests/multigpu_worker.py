@@ -37,6 +37,24 @@ def main():
         report["cases"].append({"P": P, "op": op, "exchange": exchange, "ok": ok, "got": r, "want": float(want)})
         report["ok"] &= ok
         pipe.close()
+    # sharded steps replayed from CUDA graphs (the exchange epoch advances on
+    # the device): a multi-finisher table and a single-finisher one, the
+    # result poisoned between replays
+    for (P, total, op) in [(16, 1 << 22, "sum"), (8, 1 << 20, "max")]:
+        lens = partition_sizes(total, P)
+        pipe = MapReducePipeline(lens, op=op, fused=True, world=world, rank=rank, exchange="p2p")
+        partials = [O.tree_reduce(O.map_affine(O.fill_uniform(1000 + p, lens[p]), 2.0, 1.0)
+                                  if not (p == P // 2) else _planted(p, lens[p]), op) for p in range(P)]
+        want = O.tree_reduce(np.array(partials, np.float32), op)
+        ok = True
+        for _ in range(3):
+            pipe.result.fill_(float("nan"))
+            r = float(pipe.graph_step(7).item())
+            ok &= O.f32_bits(np.float32(r)) == O.f32_bits(want)
+        ok &= pipe.exchange_error() == 0
+        report["cases"].append({"P": P, "op": op, "exchange": "p2p-graph", "ok": ok, "got": r, "want": float(want)})
+        report["ok"] &= ok
+        pipe.close()
     # C3 sharded: map_cl(pi) + reduce_cl(isum2), the rank totals exchanged
     # inside the counting kernel over NVLink; T = world - 1 leaves one rank
     # without tasks (it still joins the exchange)
@@ -57,7 +75,9 @@ def main():
         ok = got == want and hits.cpu().tolist()[:len(mine)] == [O.pi_hits(42 + t, S + 1000 * t) for t in mine]
         report["cases"].append({"pi_tasks": T, "ok": ok, "got": got, "want": want})
         report["ok"] &= ok
-    print("MULTIGPU " + json.dumps(report), flush=True)
+    # one write(2) per report: ranks share the stdout pipe, and print() may
+    # split text and newline into two writes that other ranks interleave
+    os.write(1, ("MULTIGPU " + json.dumps(report) + "\n").encode())
     dist.destroy_process_group()
     return 0 if report["ok"] else 1
 

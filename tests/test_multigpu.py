@@ -21,7 +21,12 @@ def test_sharded_pipeline_bit_identical():
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                         "--master-addr", "127.0.0.1", "--master-port", "29533",
                         str(ROOT / "tests" / "multigpu_worker.py")], capture_output=True, text=True, timeout=600)
-    lines = [l for l in r.stdout.splitlines() if l.startswith("MULTIGPU ")]
+    import json
+    import re
+
+    reports = [json.JSONDecoder().raw_decode(r.stdout, m.end())[0] for m in re.finditer(r"MULTIGPU ", r.stdout)]
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0, r.stderr[-3000:]
-    assert len(lines) == world
+    assert sorted(d["rank"] for d in reports) == list(range(world)), r.stdout[-3000:]
+    bad = [(d["rank"], c) for d in reports for c in d["cases"] if not c["ok"]]
+    assert not bad, bad
