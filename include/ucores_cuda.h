@@ -192,6 +192,13 @@ int ucg_xchg_destroy(ucg_xchg* x);
 int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, float a, float b, int op,
                               float* scratch, float* partials, ucg_xchg* xchg, float* result, void* stream);
 
+/* reduce_cl stage 2 alone, sharded: this rank's nloc partition values
+ * (device, already computed — e.g. by per-chunk launches overlapping an
+ * upload) go through the same NVLink exchange as ucg_segment_reduce_cl_f32's
+ * tail, and *result (device) is the reference pairing tree over all ranks'
+ * values in partition order. One single-CTA launch, no collective call. */
+int ucg_reduce_cl_xchg_f32(float* partials, uint64_t nloc, int op, ucg_xchg* xchg, float* result, void* stream);
+
 /* Sharded map_cl(pi) + reduce_cl(isum2) (C3 over GPUs, one process per
  * GPU): ucg_pi_hits_total over this rank's tasks, and the last CTA of the
  * launch exchanges the rank totals over NVLink (8-byte P2P stores into every

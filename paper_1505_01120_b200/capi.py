@@ -83,6 +83,7 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_pi_hits": (i32, [P(u64), P(u64), u64, vp, vp]),
     "ucg_pi_hits_total": (i32, [P(u64), P(u64), u64, vp, vp, vp]),
     "ucg_pi_hits_total_xchg": (i32, [P(u64), P(u64), u64, vp, vp, vp, vp]),
+    "ucg_reduce_cl_xchg_f32": (i32, [vp, u64, C.c_int, vp, vp, vp]),
     "ucg_pi_flags": (i32, [u64, u64, vp, vp]),
     "ucg_sobel_band_u8": (i32, [vp, vp, u64, u64, vp]),
     "ucg_sobel_bands_u8": (i32, [vp, P(u64), vp, P(u64), P(u64), u64, u64, vp]),

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -538,6 +539,15 @@ __global__ void __launch_bounds__(kTreeThreads) k_segment_finish(const __grid_co
   stage2<Op>(p, F, sm);
 }
 
+// reduce_cl stage 2 alone over partition values already in `out` (one CTA):
+// with an exchange context, the sharded NVLink exchange + the tree over all
+// ranks' values (the e2e path, whose partials come from per-chunk launches).
+template <class Op>
+__global__ void __launch_bounds__(kTreeThreads) k_stage2_only(const __grid_constant__ FinishArgs p) {
+  __shared__ TreeSmem sm;
+  stage2<Op>(p, 1, sm);
+}
+
 template <class Op>
 __global__ void __launch_bounds__(kTreeThreads) k_tree(const float* __restrict__ x, uint64_t n, float* __restrict__ out) {
   __shared__ TreeSmem sm;
@@ -997,6 +1007,30 @@ int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, flo
   if (op == UCG_OP_SUM) return segment_reduce<OpSum>(x, y, t, a, b, scratch, partials, result, xchg, as_stream(stream));
   if (op == UCG_OP_MAX) return segment_reduce<OpMax>(x, y, t, a, b, scratch, partials, result, xchg, as_stream(stream));
   return fail(UCG_ERR_ARG, "unknown op");
+}
+
+int ucg_reduce_cl_xchg_f32(float* partials, uint64_t nloc, int op, ucg_xchg* xchg, float* result, void* stream) {
+  if (int rc = check_device()) return rc;
+  if (!xchg || !result || (nloc && !partials)) return fail(UCG_ERR_ARG, "null argument");
+  if (!xchg->opened || xchg->nloc != nloc) return fail(UCG_ERR_ARG, "exchange not opened for this shard");
+  int dev = -1;
+  UCG_CUDA(cudaGetDevice(&dev));
+  if (dev != xchg->device) return fail(UCG_ERR_ARG, "exchange context belongs to another device");
+  // one CTA: the stage-2 tail with F = 1 (no ticket); done counters unused
+  static unsigned int* scratch_done[64] = {};
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!scratch_done[dev]) UCG_CUDA(cudaMalloc(&scratch_done[dev], 3 * sizeof(unsigned int)));
+  }
+  FinishArgs f{nullptr, nullptr, nloc, partials, scratch_done[dev], result, xchg->world, xchg->rank,
+               xchg->part_offset, xchg->p_total, xchg->d_peers, xchg->flags_offset, xchg->d_epoch, xchg->d_err, 0, 1};
+  cudaStream_t st = as_stream(stream);
+  if (op == UCG_OP_SUM) k_stage2_only<OpSum><<<1, kTreeThreads, 0, st>>>(f);
+  else if (op == UCG_OP_MAX) k_stage2_only<OpMax><<<1, kTreeThreads, 0, st>>>(f);
+  else return fail(UCG_ERR_ARG, "unknown op");
+  UCG_LAUNCHED();
+  return UCG_OK;
 }
 
 int ucg_tree_reduce_f32(const float* x, uint64_t n, int op, float* out, void* stream) {

@@ -196,6 +196,13 @@ class MapReducePipeline:
             ops.tree_reduce(self.partials, self.P, self.op, self.result, stream=stream)
             return self.result
         n = len(self.local_lens)
+        if self.exchange == "p2p":
+            # the fused NVLink exchange + stage-2 tree in one single-CTA launch
+            if getattr(self, "xchg", None) is None:
+                self._setup_xchg()
+            capi.call("ucg_reduce_cl_xchg_f32", self.partials.data_ptr(), n, capi.OPS[self.op], self.xchg,
+                      self.result.data_ptr(), capi.stream_handle(stream))
+            return self.result
         if self.P % self.world == 0:
             # equal blocks: the gathered buffer is already in partition order
             import torch.distributed as dist

@@ -37,6 +37,25 @@ def main():
         report["cases"].append({"P": P, "op": op, "exchange": exchange, "ok": ok, "got": r, "want": float(want)})
         report["ok"] &= ok
         pipe.close()
+    # the e2e path: per-chunk uploads + launches, then the stage-2 exchange
+    # alone (ucg_reduce_cl_xchg_f32) — p2p — or the NCCL all-gather
+    for (P, total, op, exchange) in [(16, 1 << 22, "sum", "p2p"), (7, 300001, "max", "p2p"),
+                                     (16, 1 << 22, "sum", "nccl")]:
+        lens = partition_sizes(total, P)
+        pipe = MapReducePipeline(lens, op=op, fused=True, world=world, rank=rank, exchange=exchange)
+        partials = [O.tree_reduce(O.map_affine(O.fill_uniform(1000 + p, lens[p]), 2.0, 1.0)
+                                  if not (p == P // 2) else _planted(p, lens[p]), op) for p in range(P)]
+        want = O.tree_reduce(np.array(partials, np.float32), op)
+        pipe.setup_host_input(chunks=3)
+        ok = True
+        for _ in range(3):
+            r = pipe.step_from_host()
+            ok &= O.f32_bits(np.float32(r)) == O.f32_bits(want)
+        ok &= pipe.exchange_error() == 0
+        report["cases"].append({"P": P, "op": op, "exchange": exchange + "-e2e", "ok": ok, "got": r,
+                                "want": float(want)})
+        report["ok"] &= ok
+        pipe.close()
     # sharded steps replayed from CUDA graphs (the exchange epoch advances on
     # the device): a multi-finisher table and a single-finisher one, the
     # result poisoned between replays
