@@ -288,6 +288,8 @@ struct FinishArgs {
   uint32_t* err;              // set to 1 when a wait times out
   int warp_mode;              // one warp (not one CTA) per segment
   uint32_t finishers;         // fused tail: finisher CTAs (0 = min(G, nseg))
+  int flag_exchange;          // sharded: 1 = data stores + fence + epoch flags (A/B), 0 = one
+                              // 64-bit {epoch, value} store per value, no fences
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -296,6 +298,14 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -410,7 +420,40 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
   const float* vals = p.out;
   uint64_t nvals = p.nseg;
   uint32_t epoch = 0;
-  if (p.world > 1) {
+  if (p.world > 1 && !p.flag_exchange) {
+    // Each value travels with its epoch in ONE 64-bit store to every peer's
+    // slot (single-copy atomic), so a reader that sees the epoch has the
+    // value: no system fences, no flag round trip. Slots alternate by epoch
+    // parity (a rank one step ahead writes the other buffer); the received
+    // values are unpacked into this rank's gather area for the tree.
+    epoch = *reinterpret_cast<volatile uint32_t*>(p.epoch) + 1;
+    const uint64_t buf = (epoch & 1) * p.p_total;
+    const uint64_t nsend = p.nseg * uint64_t(p.world);
+    for (uint64_t i = tid; i < nsend; i += blockDim.x) {
+      const uint64_t r = i / p.nseg, j = i - r * p.nseg;
+      uint64_t* slot = reinterpret_cast<uint64_t*>(p.peers[r]) + buf + p.part_offset + j;
+      st_relaxed_sys_u64(slot, (uint64_t(epoch) << 32) | __float_as_uint(__ldcg(p.out + j)));
+    }
+    const uint64_t* mine = reinterpret_cast<const uint64_t*>(p.peers[p.rank]) + buf;
+    float* gathered = reinterpret_cast<float*>(p.peers[p.rank] + 16 * p.p_total);
+    for (uint64_t i = tid; i < p.p_total; i += blockDim.x) {
+      uint64_t v = ld_relaxed_sys_u64(mine + i);
+      if (uint32_t(v >> 32) != epoch) {
+        const uint64_t t0 = global_ns();
+        uint32_t spins = 0;
+        while (uint32_t((v = ld_relaxed_sys_u64(mine + i)) >> 32) != epoch) {
+          if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) {  // a peer never arrived
+            atomicExch(p.err, 1u);
+            break;
+          }
+        }
+      }
+      gathered[i] = __uint_as_float(uint32_t(v));
+    }
+    __syncthreads();
+    vals = gathered;
+    nvals = p.p_total;
+  } else if (p.world > 1) {
     // this exchange's epoch and value buffer (by parity)
     epoch = *reinterpret_cast<volatile uint32_t*>(p.epoch) + 1;
     const uint64_t buf = (epoch & 1) * p.p_total;
@@ -832,7 +875,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     return fail(UCG_ERR_ARG, "segment table was created on device " + std::to_string(t->device) +
                                  ", current device is " + std::to_string(dev));
   }
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0};
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -841,6 +884,8 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.peers = xg->d_peers;
     f.flags_offset = xg->flags_offset;
     f.epoch = xg->d_epoch;
+    static const bool flags_xchg = getenv("UCG_XCHG_FLAGS") != nullptr;  // A/B: the fenced flag protocol
+    f.flag_exchange = flags_xchg ? 1 : 0;
     f.err = xg->d_err;
   }
   const bool fused_finish = t->nitems && !separate_finish();
@@ -1024,7 +1069,8 @@ int ucg_reduce_cl_xchg_f32(float* partials, uint64_t nloc, int op, ucg_xchg* xch
     if (!scratch_done[dev]) UCG_CUDA(cudaMalloc(&scratch_done[dev], 3 * sizeof(unsigned int)));
   }
   FinishArgs f{nullptr, nullptr, nloc, partials, scratch_done[dev], result, xchg->world, xchg->rank,
-               xchg->part_offset, xchg->p_total, xchg->d_peers, xchg->flags_offset, xchg->d_epoch, xchg->d_err, 0, 1};
+               xchg->part_offset, xchg->p_total, xchg->d_peers, xchg->flags_offset, xchg->d_epoch, xchg->d_err, 0, 1,
+               getenv("UCG_XCHG_FLAGS") ? 1 : 0};
   cudaStream_t st = as_stream(stream);
   if (op == UCG_OP_SUM) k_stage2_only<OpSum><<<1, kTreeThreads, 0, st>>>(f);
   else if (op == UCG_OP_MAX) k_stage2_only<OpMax><<<1, kTreeThreads, 0, st>>>(f);

@@ -389,7 +389,9 @@ int ucg_xchg_create(int world, int rank, uint64_t nloc, uint64_t part_offset, ui
   x->nloc = nloc;
   x->part_offset = part_offset;
   x->p_total = p_total;
-  x->flags_offset = (2 * p_total * 4 + 255) / 256 * 256;
+  // [2 parity buffers of p_total 64-bit {epoch, value} slots | p_total gathered
+  //  floats | pad | flags[world]] (the flag protocol uses the first 2*p_total*4 B)
+  x->flags_offset = (20 * p_total + 255) / 256 * 256;
   x->region_bytes = x->flags_offset + 256;
   x->peer_ptrs = new uint8_t*[world]();
   cudaError_t e;

@@ -21,7 +21,7 @@ def per_step(fn, k, reps=5):
     return best
 
 
-for G in (8, 4, 1):
+for G in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["8", "4", "1"])]:
     P = 64 // G
     pipe = MapReducePipeline([1 << 24] * P, plant_max=False)
     K = 20
