@@ -85,8 +85,11 @@ def run(args, world, rank, local):
     cpu = None
     line = None
     if args.workload == "c1":
+        # C1 is too small to shard — at N > 1 every GPU runs the
+        # whole 2^20-element collection as an independent replica (weak
+        # scaling: value = all replicas' elements / max-over-ranks time)
         lens = [1 << 18] * 4
-        pipe = MapReducePipeline(lens, world=world, rank=rank, device=dev, plant_max=False)
+        pipe = MapReducePipeline(lens, world=1, rank=0, device=dev, plant_max=False)
         for _ in range(w):
             pipe.step()
         # the K timed steps replayed from ONE CUDA graph of K one-kernel steps:
@@ -109,7 +112,7 @@ def run(args, world, rank, local):
             pipe.step_from_host()
         e2e_ms = _timed(pipe.step_from_host, k, barrier)
         ms, kern, e2e_ms = _max_over_ranks([ms, kern, e2e_ms], world, dev)
-        n = pipe.elements
+        n = pipe.elements * world  # replicas
         if rank == 0 and world == 1:
             r = B.run_ref_harness(4, 1 << 18, 3, 1, "sum", os.cpu_count() or 1)
             cpu = {"value": r["elements"] / statistics.median(r["step_s"]), "unit": "elements/s",
@@ -121,7 +124,10 @@ def run(args, world, rank, local):
                      {"bound": "latency", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                       "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
                       "note": "4 MiB collection: L2-resident and launch-latency bound (1 kernel per step; the K steps replayed from one CUDA graph with programmatic-dependent-launch edges); no HBM claim"},
-                     cpu, {"workload": CONFIGS[0], "elements": n, "partitions": 4, "dtype": "f32", "fused": True})
+                     cpu, {"workload": CONFIGS[0], "elements": n, "partitions": 4, "dtype": "f32", "fused": True,
+                           "sharding": "replicas: every GPU runs the whole collection" if world > 1 else "1 GPU"})
+        if world > 1:
+            line["scaling"] = "weak"
         pipe.close()
     elif args.workload == "c3":
         S, T = 1 << 34, 64
