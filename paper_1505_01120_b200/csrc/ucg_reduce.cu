@@ -290,6 +290,8 @@ struct FinishArgs {
   uint32_t finishers;         // fused tail: finisher CTAs (0 = min(G, nseg))
   int flag_exchange;          // sharded: 1 = data stores + fence + epoch flags (A/B), 0 = one
                               // 64-bit {epoch, value} store per value, no fences
+  int early_send;             // sharded, 64-bit protocol: each finisher sends its partition
+                              // values as it computes them (stage 2 only receives)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -350,8 +352,20 @@ __device__ float warp_tree(const float* __restrict__ vals, uint64_t n, int lane)
 
 // Partition values of segments j, j+F, j+2F, ... (one CTA = finisher j of F),
 // or — with many partitions of few items (warp_mode) — one warp per segment.
+// Sharded, 64-bit protocol: partition value s of this rank to every peer's
+// slot, tagged with this exchange's epoch (the counter advances only after
+// every finisher has passed stage 2's ticket, so all finishers read the same).
+__device__ __forceinline__ void send_value(const FinishArgs& p, uint64_t s, float r) {
+  const uint32_t e = *reinterpret_cast<volatile uint32_t*>(p.epoch) + 1;
+  const uint64_t buf = (e & 1) * p.p_total;
+  for (int q = 0; q < p.world; ++q)
+    st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(p.peers[q]) + buf + p.part_offset + s,
+                       (uint64_t(e) << 32) | __float_as_uint(r));
+}
+
 template <class Op>
 __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm) {
+  const bool send = p.world > 1 && p.early_send;
   if (p.warp_mode) {
     const int lane = threadIdx.x & 31;
     for (uint64_t s = j * kWarps + (threadIdx.x >> 5); s < p.nseg; s += F * kWarps) {
@@ -360,6 +374,7 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
       if (lane == 0) {
         __stcg(p.out + s, r);
         if (F == 1 && s < 32) sm.seg[s] = r;
+        if (send) send_value(p, s, r);
       }
     }
     return;
@@ -367,7 +382,10 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
   for (uint64_t s = j; s < p.nseg; s += F) {
     const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
     const float r = n ? cta_tree<Op>(p.partial + f, n, sm) : Op::empty();
-    if (threadIdx.x == 0) __stcg(p.out + s, r);
+    if (threadIdx.x == 0) {
+      __stcg(p.out + s, r);
+      if (send) send_value(p, s, r);
+    }
   }
 }
 
@@ -428,7 +446,7 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
     // values are unpacked into this rank's gather area for the tree.
     epoch = *reinterpret_cast<volatile uint32_t*>(p.epoch) + 1;
     const uint64_t buf = (epoch & 1) * p.p_total;
-    const uint64_t nsend = p.nseg * uint64_t(p.world);
+    const uint64_t nsend = p.early_send ? 0 : p.nseg * uint64_t(p.world);  // early: sent by the finishers
     for (uint64_t i = tid; i < nsend; i += blockDim.x) {
       const uint64_t r = i / p.nseg, j = i - r * p.nseg;
       uint64_t* slot = reinterpret_cast<uint64_t*>(p.peers[r]) + buf + p.part_offset + j;
@@ -875,7 +893,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     return fail(UCG_ERR_ARG, "segment table was created on device " + std::to_string(t->device) +
                                  ", current device is " + std::to_string(dev));
   }
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0};
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -885,7 +903,9 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.flags_offset = xg->flags_offset;
     f.epoch = xg->d_epoch;
     static const bool flags_xchg = getenv("UCG_XCHG_FLAGS") != nullptr;  // A/B: the fenced flag protocol
+    static const bool late_send = getenv("UCG_XCHG_LATE_SEND") != nullptr;  // A/B: stage 2 sends everything
     f.flag_exchange = flags_xchg ? 1 : 0;
+    f.early_send = (flags_xchg || late_send) ? 0 : 1;
     f.err = xg->d_err;
   }
   const bool fused_finish = t->nitems && !separate_finish();
@@ -1070,7 +1090,7 @@ int ucg_reduce_cl_xchg_f32(float* partials, uint64_t nloc, int op, ucg_xchg* xch
   }
   FinishArgs f{nullptr, nullptr, nloc, partials, scratch_done[dev], result, xchg->world, xchg->rank,
                xchg->part_offset, xchg->p_total, xchg->d_peers, xchg->flags_offset, xchg->d_epoch, xchg->d_err, 0, 1,
-               getenv("UCG_XCHG_FLAGS") ? 1 : 0};
+               getenv("UCG_XCHG_FLAGS") ? 1 : 0, 0};
   cudaStream_t st = as_stream(stream);
   if (op == UCG_OP_SUM) k_stage2_only<OpSum><<<1, kTreeThreads, 0, st>>>(f);
   else if (op == UCG_OP_MAX) k_stage2_only<OpMax><<<1, kTreeThreads, 0, st>>>(f);
