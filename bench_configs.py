@@ -125,6 +125,7 @@ def run(args, world, rank, local):
                       "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
                       "note": "4 MiB collection: L2-resident and launch-latency bound (1 kernel per step; the K steps replayed from one CUDA graph with programmatic-dependent-launch edges); no HBM claim"},
                      cpu, {"workload": CONFIGS[0], "elements": n, "partitions": 4, "dtype": "f32", "fused": True,
+                           "l2": "no flush: the 4 MiB collection is L2-resident by size (latency-bound case, not the headline)",
                            "sharding": "replicas: every GPU runs the whole collection" if world > 1 else "1 GPU"})
         if world > 1:
             line["scaling"] = "weak"
@@ -184,6 +185,7 @@ def run(args, world, rank, local):
                       "frac": achieved / ipc_peak, "traffic": 0, "note": "integer-ALU / issue bound; no HBM traffic"},
                      cpu, {"workload": CONFIGS[2], "samples": S, "tasks": T, "dtype": "u64/f64->i64",
                            "hits_total": total_hits,
+                           "l2": "n/a: no input data (samples generated in registers)",
                            "exchange": "none" if world == 1 else "rank totals exchanged inside the counting kernel over NVLink (P2P stores + epoch flags)"})
     elif args.workload == "c4":
         H = W = 16384
@@ -226,7 +228,7 @@ def run(args, world, rank, local):
                       "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
                       "algorithmic_bytes_per_launch": algo},
                      cpu, {"workload": CONFIGS[3], "height": H, "width": W, "bands": nb, "rows_per_band": R,
-                           "dtype": "u8"})
+                           "dtype": "u8", "l2": "inputs larger than L2 (257 MiB image in, 256 MiB out)"})
     elif args.workload == "c5":
         # BASELINE: "dense fp32 matrix multiply ... tensor-core path". The line's
         # value is the fp32-faithful product (ucg_gemm_f32: 3xTF32 split on the
@@ -301,7 +303,8 @@ def run(args, world, rank, local):
                      cpu, {"workload": CONFIGS[4], "n": n, "partitions": P,
                            "dtype": "f32 (fp32-faithful: 3xTF32 split on tcgen05, fp32 accumulate, k-chunks of 256 "
                                     "added in fp32 round-to-nearest)",
-                           "max_abs_err_over_rms_256_sampled": err32})
+                           "max_abs_err_over_rms_256_sampled": err32,
+                           "l2": "inputs larger than L2 (8 partitions x 512 MiB A||B per step)"})
         line["tf32"] = {
             "value": flops / (mstf * 1e-3), "unit": "FLOP/s", "ms_per_step": mstf, "kernel": "ucg_gemm_tf32",
             "roofline_frac": tctf / peak, "max_abs_err_over_rms_256_sampled": errtf,
@@ -408,7 +411,8 @@ def run(args, world, rank, local):
                       "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
                       "algorithmic_bytes_per_launch": algo},
                      cpu, {"workload": "1 GiB synthetic text in 64 chunks of 16 MiB, word-start flags (u8 per byte)",
-                           "bytes": total, "chunks": chunks, "dtype": "u8", "word_starts_this_rank": words})
+                           "bytes": total, "chunks": chunks, "dtype": "u8", "word_starts_this_rank": words,
+                           "l2": "inputs larger than L2 (1 GiB text)"})
     if rank == 0 and line is not None:
         B.emit(line)
     if world > 1:
