@@ -125,6 +125,7 @@ struct ucg_segtab {
   uint64_t max_items_per_seg;
   int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
   uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches)
+  uint64_t ntaper;         // trailing items the fused map streams as 4 sub-items each (0: none)
 };
 
 // Peer-exchange context of a sharded reduce_cl (one process per GPU).

@@ -292,6 +292,8 @@ struct FinishArgs {
                               // 64-bit {epoch, value} store per value, no fences
   int early_send;             // sharded, 64-bit protocol: each finisher sends its partition
                               // values as it computes them (stage 2 only receives)
+  float* sub;                 // tapered tail: 4 sub-item roots per item in [taper_first, +ntaper)
+  uint64_t taper_first, ntaper;
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -363,6 +365,18 @@ __device__ __forceinline__ void send_value(const FinishArgs& p, uint64_t s, floa
                        (uint64_t(e) << 32) | __float_as_uint(r));
 }
 
+// Tapered tail: the item roots of segment items [f, f+n) that were streamed
+// as 4 aligned sub-items, rebuilt as ((s0, s1), (s2, s3)) — the association
+// work_item gives a whole item of 4 sub-item-sized subtrees.
+template <class Op>
+__device__ __forceinline__ void taper_roots(const FinishArgs& p, uint64_t f, uint64_t n, uint32_t t, uint32_t nt) {
+  const uint64_t lo = f > p.taper_first ? f : p.taper_first;
+  for (uint64_t i = lo + t; i < f + n; i += nt) {
+    const float4 q = __ldcg(reinterpret_cast<const float4*>(p.sub) + (i - p.taper_first));
+    __stcg(const_cast<float*>(p.partial) + i, Op::apply(Op::apply(q.x, q.y), Op::apply(q.z, q.w)));
+  }
+}
+
 template <class Op>
 __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm) {
   const bool send = p.world > 1 && p.early_send;
@@ -370,6 +384,10 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
     const int lane = threadIdx.x & 31;
     for (uint64_t s = j * kWarps + (threadIdx.x >> 5); s < p.nseg; s += F * kWarps) {
       const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
+      if (p.ntaper && f + n > p.taper_first) {
+        taper_roots<Op>(p, f, n, lane, 32);
+        __syncwarp();
+      }
       const float r = n ? warp_tree<Op>(p.partial + f, n, lane) : Op::empty();
       if (lane == 0) {
         __stcg(p.out + s, r);
@@ -381,6 +399,10 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
   }
   for (uint64_t s = j; s < p.nseg; s += F) {
     const uint64_t f = p.first_item[s], n = p.first_item[s + 1] - f;
+    if (p.ntaper && f + n > p.taper_first) {
+      taper_roots<Op>(p, f, n, threadIdx.x, blockDim.x);
+      __syncthreads();
+    }
     const float r = n ? cta_tree<Op>(p.partial + f, n, sm) : Op::empty();
     if (threadIdx.x == 0) {
       __stcg(p.out + s, r);
@@ -545,11 +567,29 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   // two for the read-only reduction, whose items finish twice as fast and
   // would otherwise saturate the single claim counter.
   constexpr uint64_t kPer = kMap ? 1 : 2;
+  // Tapered tail (map stream only): units past taper_first are sub-items, a
+  // quarter of an item each, so the last warps finish close together.
+  const uint64_t ntaper = kMap ? p.fin.ntaper : 0;
+  const uint64_t units_end = ntaper ? p.fin.taper_first + 4 * ntaper : 0;
   uint64_t unit = warp;
-  while (unit * kPer < p.nitems) {
+  while (ntaper ? unit < units_end : unit * kPer < p.nitems) {
     // dynamic: the next unit is claimed now and consumed after this one
     uint32_t claim = 0;
     if (p.dynamic && lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
+    if (ntaper && unit >= p.fin.taper_first) {
+      const uint64_t u = unit - p.fin.taper_first, item = p.fin.taper_first + (u >> 2);
+      const uint32_t s = p.item_seg[item];
+      const int sl = p.item_log2 - 2;
+      const uint64_t start = ((item - p.first_item[s]) << p.item_log2) + ((u & 3) << sl);
+      const uint64_t off = p.begin[s] + start;
+      const int64_t valid = int64_t(p.len[s]) - int64_t(start);  // <= 0: an empty sub-item
+      const float r = work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr,
+                                             valid < (int64_t(1) << sl) ? valid : (int64_t(1) << sl),
+                                             int64_t(1) << sl, p.a, p.b, lane);
+      if (lane == 0) p.fin.sub[u] = r;
+      unit = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : unit + nwarps;
+      continue;
+    }
 #pragma unroll 1
     for (uint64_t item = unit * kPer; item < umin((unit + 1) * kPer, p.nitems); ++item) {
       const uint32_t s = p.item_seg[item];
@@ -907,6 +947,11 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.flag_exchange = flags_xchg ? 1 : 0;
     f.early_send = (flags_xchg || late_send) ? 0 : 1;
     f.err = xg->d_err;
+  }
+  if (y && t->ntaper) {  // tapered tail of the map stream (scratch: item roots, then the sub-roots)
+    f.sub = scratch + ((t->nitems + 4) & ~uint64_t(3));  // 16-byte aligned
+    f.taper_first = t->nitems - t->ntaper;
+    f.ntaper = t->ntaper;
   }
   const bool fused_finish = t->nitems && !separate_finish();
   // many partitions of few items: a warp per partition tree (the fused tail

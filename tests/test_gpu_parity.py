@@ -511,3 +511,23 @@ def test_engine_capi_pi(cuda, golden):
     case = golden["pi"][0]
     hits, _ = engine_capi.pi(case["samples"], case["tasks"], case["seed"])
     assert hits == case["hits"]
+
+
+def test_tapered_tail_bitexact():
+    """UCG_TAPER (A/B knob, off by default): the fused map's last items are
+    streamed as 4 sub-items and the finishers recombine the sub-roots. The
+    fused cases — many ragged/empty partitions (warp-per-partition tail),
+    SEG_LENS, and full-size C2 (CTA-per-partition tail) — rerun in a fresh
+    process with the knob on must stay bit-exact (the knob is read once per
+    process)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, UCG_TAPER="64")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f"{__file__}::test_many_partitions_bitexact", f"{__file__}::test_fused_map_reduce_bitexact",
+                        f"{__file__}::test_c2_full_size", "-k", "True or fused_map or full_size"],
+                       env=env, cwd=os.path.dirname(__file__), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "5 passed" in r.stdout, r.stdout[-2000:]
