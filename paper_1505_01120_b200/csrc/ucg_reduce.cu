@@ -876,7 +876,13 @@ cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_
   // that launch instead overlaps its ramp with the previous step's tail
   // (programmatic dependent launch; C1: the whole step is ~6 us)
   static const bool no_pdl = getenv("UCG_NO_PDL") != nullptr;
-  if (args.finish && args.fin.finishers != 1) {
+  // UCG_PDL_MULTI=1 (A/B): the multi-finisher launch too is a PDL launch
+  // instead of a cooperative one. Its grid never exceeds the co-resident
+  // capacity (2 CTAs x 148 SMs at the occupancy the cooperative launch
+  // validates), and the next step's CTAs park in griddepcontrol.wait only in
+  // slots this grid has left, so every CTA of this grid is already resident.
+  static const bool pdl_multi = getenv("UCG_PDL_MULTI") != nullptr;
+  if (args.finish && args.fin.finishers != 1 && !(pdl_multi && !no_pdl)) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.numAttrs = 1;
