@@ -79,7 +79,10 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="launch the K timed steps one by one")
     ap.add_argument("--workload", default="c2", choices=["c1", "c1lit", "c2", "c3", "c4", "c5", "wc"],
                     help="c2 (default) is the headline; the others are the remaining BASELINE configs")
-    ap.add_argument("--cpu-sample-parts", type=int, default=4)
+    ap.add_argument("--cpu-sample-parts", type=int, default=4,
+                    help="partitions in our arm's bounded cpu_baseline sample")
+    ap.add_argument("--ref-parts", type=int, default=0,
+                    help="--impl reference: partitions timed (default 0 = the whole --parts workload)")
     return ap.parse_args()
 
 
@@ -88,6 +91,34 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_under_torchrun(args) -> int | None:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this command
+    as N ranks (one process per GPU) under torch.distributed.run on 127.0.0.1.
+    Returns the launcher's exit code, or None when no relaunch is needed. Our
+    arm fails loudly when fewer than N GPUs are visible."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl == "ours":
+        import torch
+
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {n} GPU(s) visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve())]
+    return subprocess.call(cmd + sys.argv[1:])
 
 
 # ---- reference arm / cpu baseline --------------------------------------------------
@@ -122,26 +153,34 @@ def cpu_model() -> str:
 
 
 def reference_arm(args, world, rank):
+    """The reference's own CPU implementation of the path, on the SAME workload
+    as our arm (all args.parts partitions, the planted maximum included) —
+    one step = the whole map_cl -> map_cl_partition -> reduce_cl chain over
+    the whole collection. Rank 0 alone runs it; other ranks exit 0."""
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    parts = args.cpu_sample_parts
+    parts = args.ref_parts or args.parts
     r = run_ref_harness(parts, args.part_len, args.steps, args.warmup, args.op, threads)
     elems = r["elements"]
-    step = statistics.median(r["step_s"])
+    step = statistics.fmean(r["step_s"])
     value = elems / step
-    sample = (f"{parts} partitions x {args.part_len} fp32 ({elems} elements; same partition size as the "
-              f"{args.parts}-partition workload), {r['executor']} width {threads}, {cpu_model()}")
+    cfg = workload_config(args, world)
+    if parts != args.parts:  # an explicitly requested sample: say so in the config
+        cfg = cfg | {"elements": elems, "partitions": parts,
+                     "sample": f"{parts} of the {args.parts} partitions (--ref-parts)"}
+    sample = (f"{parts} partitions x {args.part_len} fp32 ({elems} elements), {r['executor']} width {threads}, "
+              f"{cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {k: v for k, v in workload_config(args, world=1).items()
-                   if k in ("workload", "elements", "partitions", "part_len")} | {
-            "path": "unmodified ucores Engine + WorkerRuntime + host executor (oracle/_ref), host threads"},
+        "config": cfg,
+        "reference_path": "unmodified ucores Engine + WorkerRuntime + HostParallelExecutor (oracle/_ref/ref_harness, "
+                          "compiled from the reference headers) over all host threads",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "result_bits": r["result_bits"],
+        "result_bits": r["result_bits"], "result": r.get("result"),
     }
     emit(line)
     return 0
@@ -222,6 +261,31 @@ def workload_config(args, world: int) -> dict:
     }
 
 
+GOLDEN_FULL = ROOT / "tests" / "golden" / "ref_golden_full.json"
+
+
+def reference_parity(args, pipe, result: float) -> dict | None:
+    """The timed step's result (and this rank's partition values) against the
+    reference's own output at the BASELINE C2 size (tests/golden/
+    ref_golden_full.json, made by the unmodified reference Engine); None for
+    other shapes."""
+    import numpy as np
+
+    try:
+        g = json.loads(GOLDEN_FULL.read_text())["c2_full"]
+    except Exception:
+        return None
+    if (args.parts, args.part_len) != (g["P"], g["L"]):
+        return None
+    bits = lambda v: "%08x" % int(np.array([v], np.float32).view(np.uint32)[0])
+    mine = [bits(v) for v in pipe.partials.cpu().numpy()[:len(pipe.local_lens)]]
+    want = [g[f"partials_{args.op}"][p] for p in pipe.owned]
+    return {"reference": "tests/golden/ref_golden_full.json (unmodified reference Engine, same input)",
+            "result_bits": bits(result), "reference_result_bits": g[f"total_{args.op}"],
+            "result_match": bits(result) == g[f"total_{args.op}"],
+            "partials_match": mine == want, "partials_checked": len(mine)}
+
+
 def load_peak() -> tuple[float, str]:
     try:
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
@@ -294,6 +358,7 @@ def our_arm(args, world, rank, local):
         # graph replays bypass the C launch counter: one k_segment_pass1 node per step
         launches = k if not args.no_graph else capi.launch_count() - launches0
         result = float(pipe.result.item())
+        parity = reference_parity(args, pipe, result)
         # timed region 2 (roofline): K launches of the dominant kernel (the
         # fused map + partition reduce, trees in its tail), one event pair each
         barrier()
@@ -397,7 +462,7 @@ def our_arm(args, world, rank, local):
             engine_e2e = {"value": None, "error": str(e)[:300]}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
             r = run_ref_harness(args.cpu_sample_parts, args.part_len, 1, 0, args.op, threads)
@@ -435,6 +500,7 @@ def our_arm(args, world, rank, local):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "result": result,
+            "parity": parity,
         }
         emit(line)
     pipe.close()
@@ -447,7 +513,13 @@ def our_arm(args, world, rank, local):
 
 def main():
     args = parse()
+    rc = relaunch_under_torchrun(args)  # the parent's stdout passes through to rank 0
+    if rc is not None:
+        return rc
+    _claim_stdout()
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         return reference_arm(args, world, rank)
     if args.workload != "c2":
@@ -458,5 +530,4 @@ def main():
 
 
 if __name__ == "__main__":
-    _claim_stdout()
     sys.exit(main())

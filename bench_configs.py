@@ -113,7 +113,7 @@ def run(args, world, rank, local):
         e2e_ms = _timed(pipe.step_from_host, k, barrier)
         ms, kern, e2e_ms = _max_over_ranks([ms, kern, e2e_ms], world, dev)
         n = pipe.elements * world  # replicas
-        if rank == 0 and world == 1:
+        if rank == 0:
             r = B.run_ref_harness(4, 1 << 18, 3, 1, "sum", os.cpu_count() or 1)
             cpu = {"value": r["elements"] / statistics.median(r["step_s"]), "unit": "elements/s",
                    "cores": os.cpu_count(), "kind": "reference", "sample": "the full C1 workload (2^20 fp32, 4 partitions)"}
@@ -171,7 +171,7 @@ def run(args, world, rank, local):
             chk = hits.sum().reshape(1).clone()
             dist.all_reduce(chk)
             assert int(chk.item()) == total_hits, (int(chk.item()), total_hits)
-        if rank == 0 and world == 1:
+        if rank == 0:
             r = _ref_workload(["--w", "pi", "--samples", str(1 << 28), "--tasks", "64", "--steps", "1", "--warmup", "0"])
             cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "samples/s", "cores": r["threads"],
                    "kind": "reference", "sample": "2^28 samples in 64 tasks (the C3 task shape, 1/64 of the samples)"}
@@ -214,7 +214,7 @@ def run(args, world, rank, local):
             torch.cuda.current_stream().synchronize()
         e2e_ms = _timed(e2e, k, barrier)
         ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
-        if rank == 0 and world == 1:
+        if rank == 0:
             r = _ref_workload(["--w", "sobel", "--height", "2048", "--width", str(W), "--rows", str(R), "--steps", "1",
                                "--warmup", "0"])
             cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "pixels/s", "cores": r["threads"],
@@ -284,7 +284,7 @@ def run(args, world, rank, local):
         e2e_ms = _timed(e2e, max(1, k // 4), barrier)
         ms32, mstf, cub, e2e_ms = _max_over_ranks([ms32, mstf, cub, e2e_ms], world, dev)
         flops = 2.0 * n ** 3 * P
-        if rank == 0 and world == 1:
+        if rank == 0:
             r = _ref_workload(["--w", "matmul", "--n", "256", "--parts", "2", "--steps", "1", "--warmup", "0"])
             cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "FLOP/s", "cores": r["threads"],
                    "kind": "reference", "sample": "2 partitions at n=256 (the fp32 class-D run(); 8192^3 is infeasible on CPU)"}
@@ -394,7 +394,7 @@ def run(args, world, rank, local):
         e2e_ms = _timed(e2e, k, barrier)
         ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
         words = int(flags.sum(dtype=torch.int64).item()) if ln else 0
-        if rank == 0 and world == 1:
+        if rank == 0:
             r = _ref_workload(["--w", "wordcount", "--bytes", str(1 << 26), "--chunk", str(1 << 22), "--steps", "1",
                                "--warmup", "0"])
             cpu = {"value": r["units"] / statistics.median(r["step_s"]), "unit": "bytes/s", "cores": r["threads"],

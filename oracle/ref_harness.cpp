@@ -761,6 +761,113 @@ json run_golden() {
   return g;
 }
 
+// ---- golden-full ----------------------------------------------------------------
+
+// The reference's own results at the BASELINE.json sizes (run with the host
+// parallel executor; every kernel is class D, so the results do not depend on
+// the executor):
+//   C2  2^30 fp32 in 64 partitions of 2^24 (partition p from seed 1000+p, the
+//       planted unique maximum 1.5 in partition 32 at index L/3):
+//       map_cl(axpb) -> map_cl_partition(psum|pmax) -> reduce_cl(sum2|max2);
+//       per-partition FNV-1a of y, all 64 partials and the result bits
+//   C3  2^34 samples, 64 tasks of 2^28, task seed 42+t: all 64 hit counts
+//   C4  16384^2 u8 (seed 7), 64 bands of 256 rows with halos: per-band and
+//       whole-output FNV-1a
+json run_golden_full(unsigned threads, const std::string& which) {
+  json g;
+  g["generator"] = "oracle/ref_harness.cpp golden-full (reference ucores headers, host-par executor)";
+  g["threads"] = threads;
+  auto want = [&](const char* w) { return which == "all" || which == w; };
+  if (want("c2")) {
+    const std::size_t P = 64, L = 1u << 24;
+    KernelRegistry reg = make_registry(16, 16);
+    DirectDriver drv(reg, host_device(threads));
+    Engine eng(drv, reg);
+    Dataset x;
+    {
+      std::vector<Element> es;
+      es.reserve(P);
+      for (std::size_t p = 0; p < P; ++p) {
+        std::vector<float> v(L);
+        for (std::size_t i = 0; i < L; ++i) v[i] = uniform01(1000 + p, i);
+        if (p == P / 2) v[L / 3] = 1.5f;
+        es.push_back(Element::f32(std::move(v)));
+      }
+      x = create_dataset(std::move(es), P);
+    }
+    Dataset y = eng.map_cl(x, "axpb");
+    x = Dataset();
+    json c;
+    c["P"] = P;
+    c["L"] = L;
+    c["planted_max"] = {{"partition", P / 2}, {"index", L / 3}, {"value", 1.5}};
+    std::vector<std::string> yf;
+    for (const Element& e : y.collect()) yf.push_back(hex64(fnv64(e.as_f32().data(), e.as_f32().size_bytes())));
+    c["y_fnv"] = yf;
+    for (const char* op : {"sum", "max"}) {
+      Dataset ps = eng.map_cl_partition(y, std::string("p") + op);
+      std::vector<std::string> pbits;
+      for (const Element& e : ps.collect()) pbits.push_back(hexf(e.as_f32()[0]));
+      Element r = eng.reduce_cl(ps, std::string(op) + "2");
+      c[std::string("partials_") + op] = pbits;
+      c[std::string("total_") + op] = hexf(r.as_f32()[0]);
+      c[std::string("total_") + op + "_value"] = r.as_f32()[0];
+    }
+    g["c2_full"] = c;
+  }
+  if (want("c3")) {
+    const std::uint64_t S = 1ull << 34, T = 64;
+    KernelRegistry reg = make_registry(16, 16);
+    DirectDriver drv(reg, host_device(threads));
+    Engine eng(drv, reg);
+    std::vector<Element> es;
+    for (std::uint64_t t = 0; t < T; ++t)
+      es.push_back(Element::i64({static_cast<std::int64_t>(42 + t), static_cast<std::int64_t>(S / T)}));
+    Dataset d = create_dataset(std::move(es), T);
+    Dataset r = eng.map_cl(d, "pi");
+    std::vector<std::int64_t> hits;
+    std::int64_t total = 0;
+    for (const Element& e : r.collect()) {
+      hits.push_back(e.as_i64()[0]);
+      total += e.as_i64()[0];
+    }
+    // reduce_cl(isum2) over the {hits, samples} pairs, as the GPU path folds it
+    Element tot = eng.reduce_cl(r, "isum2");
+    g["c3_full"] = {{"samples", S}, {"tasks", T}, {"seed", 42}, {"task_hits", hits}, {"hits", total},
+                    {"reduce_cl_isum2", std::vector<std::int64_t>(tot.as_i64().begin(), tot.as_i64().end())}};
+  }
+  if (want("c4")) {
+    const std::size_t H = 16384, W = 16384, R = 256;
+    KernelRegistry reg = make_registry(W, 16);
+    DirectDriver drv(reg, host_device(threads));
+    Engine eng(drv, reg);
+    std::vector<std::vector<std::uint8_t>> bands;
+    {
+      auto img = sobel_image(H, W, 7);
+      bands = sobel_bands(img, H, W, R);
+    }
+    std::vector<Element> es;
+    for (auto& b : bands) es.push_back(Element::bytes(std::move(b)));
+    bands.clear();
+    const std::size_t nb = es.size();
+    Dataset d = create_dataset(std::move(es), nb);
+    Dataset r = eng.map_cl_partition(d, "sobel");
+    std::vector<std::string> bf;
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (const Element& e : r.collect()) {
+      auto v = e.as_bytes();
+      bf.push_back(hex64(fnv64(v.data(), v.size())));
+      for (std::uint8_t b : v) {
+        h ^= b;
+        h *= 0x100000001b3ull;
+      }
+    }
+    g["c4_full"] = {{"H", H}, {"W", W}, {"rows", R}, {"seed", 7}, {"bands", nb}, {"band_fnv", bf},
+                    {"fnv", hex64(h)}};
+  }
+  return g;
+}
+
 // ---- bench -------------------------------------------------------------------
 
 // Bounded CPU samples of the other BASELINE configs through the reference
@@ -904,6 +1011,7 @@ int run_bench_literal(int argc, char** argv) {
 
 int run_bench(int argc, char** argv) {
   std::size_t P = 4, L = 1u << 24;
+  bool plant = true;
   unsigned threads = std::thread::hardware_concurrency();
   int steps = 3, warmup = 1;
   std::string op = "sum";
@@ -916,6 +1024,7 @@ int run_bench(int argc, char** argv) {
     else if (k == "--steps") steps = std::stoi(v);
     else if (k == "--warmup") warmup = std::stoi(v);
     else if (k == "--op") op = v;
+    else if (k == "--plant") plant = std::stoi(v) != 0;
   }
   KernelRegistry reg = make_registry(16, 16);
   DirectDriver drv(reg, host_device(threads));
@@ -923,6 +1032,8 @@ int run_bench(int argc, char** argv) {
   std::vector<std::vector<float>> es(P, std::vector<float>(L));
   for (std::size_t p = 0; p < P; ++p)
     for (std::size_t i = 0; i < L; ++i) es[p][i] = uniform01(1000 + p, i);
+  // the planted unique maximum of bench.py's C2 input (partition P/2, index L/3)
+  if (plant) es[P / 2][L / 3] = 1.5f;
   Dataset x = f32_dataset(es, P);
   es.clear();
   std::vector<double> times;
@@ -943,6 +1054,7 @@ int run_bench(int argc, char** argv) {
   out["threads"] = threads;
   out["executor"] = threads <= 1 ? "host-seq" : "host-par";
   out["op"] = op;
+  out["planted_max"] = plant;
   out["step_s"] = times;
   out["result_bits"] = hexf(result);
   out["result"] = result;
@@ -957,6 +1069,17 @@ int main(int argc, char** argv) {
   try {
     if (mode == "golden") {
       std::cout << run_golden().dump(1) << std::endl;
+      return 0;
+    }
+    if (mode == "golden-full") {
+      unsigned threads = std::thread::hardware_concurrency();
+      std::string which = "all";
+      for (int i = 2; i + 1 < argc; i += 2) {
+        const std::string k = argv[i], v = argv[i + 1];
+        if (k == "--threads") threads = static_cast<unsigned>(std::stoul(v));
+        else if (k == "--which") which = v;
+      }
+      std::cout << run_golden_full(threads, which).dump(1) << std::endl;
       return 0;
     }
     if (mode == "bench") return run_bench(argc, argv);

@@ -11,6 +11,9 @@ check the whole result or a stated sample of it in seconds:
   C5  8192^3 TF32: 64 sampled output entries within the TF32 tolerance of an
       fp64 dot product of the same fp32 inputs
 """
+import json
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -18,6 +21,47 @@ import oracle_lib as O
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
+
+# the reference's own output at the BASELINE sizes (tests/golden/make_golden_full.py)
+FULL = json.loads((Path(__file__).resolve().parent / "golden" / "ref_golden_full.json").read_text())
+
+
+@pytest.mark.parametrize("op,fused", [("sum", True), ("max", True), ("sum", False)])
+def test_c2_full_vs_reference(cuda, op, fused):
+    """C2 (2^30 fp32, 64 partitions, planted maximum): every partition's y, all
+    64 partials and the reduce_cl result bit-identical to the unmodified
+    reference Engine's output at this size."""
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    g = FULL["c2_full"]
+    P, L = g["P"], g["L"]
+    pipe = MapReducePipeline([L] * P, op=op, fused=fused, plant_max=True)
+    pipe.result.fill_(float("nan"))
+    r = pipe.step()
+    assert O.f32_bits(r.cpu().numpy()[0]) == g[f"total_{op}"]
+    got = [O.f32_bits(v) for v in pipe.partials.cpu().numpy()[:P]]
+    assert got == g[f"partials_{op}"]
+    if op == "sum" and fused:
+        for p in range(P):
+            assert O.fnv64(pipe.local_output(p).cpu().numpy()) == g["y_fnv"][p], p
+    # the graph-replayed step (as bench.py times it) gives the same bits
+    pipe.result.fill_(float("nan"))
+    assert O.f32_bits(pipe.graph_step(3).cpu().numpy()[0]) == g[f"total_{op}"]
+    pipe.close()
+
+
+def test_c3_full_vs_reference(cuda):
+    """C3 (2^34 samples, 64 tasks, seed 42+t): all 64 task hit counts and the
+    reduce_cl(isum2) total equal the reference's."""
+    from paper_1505_01120_b200 import ops
+
+    g = FULL["c3_full"]
+    S, T = g["samples"], g["tasks"]
+    hits = torch.empty(T, dtype=torch.int64, device=cuda)
+    total = torch.empty(1, dtype=torch.int64, device=cuda)
+    ops.pi_hits([g["seed"] + t for t in range(T)], [S // T] * T, hits, total_out=total)
+    assert hits.cpu().tolist() == g["task_hits"]
+    assert int(total.item()) == g["reduce_cl_isum2"][0] == g["hits"]
 
 
 def test_c1_full(cuda):
@@ -96,6 +140,11 @@ def test_c4_full(cuda):
         assert np.array_equal(out[b].cpu().numpy().reshape(-1), want.reshape(-1))
     for b in range(nb):
         assert torch.equal(out[b], _sobel_torch(inp[b].reshape(-1), R, W))
+    # every band equals the reference's own output at this size (FNV-1a)
+    g = FULL["c4_full"]
+    assert (g["H"], g["W"], g["rows"], g["seed"]) == (H, W, R, 7)
+    host = out.cpu().numpy()
+    assert [O.fnv64(host[b]) for b in range(nb)] == g["band_fnv"]
 
 
 def test_c5_full_sampled(cuda):

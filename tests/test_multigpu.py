@@ -17,7 +17,7 @@ def test_sharded_pipeline_bit_identical():
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    world = min(n, 4)
+    world = n  # every visible GPU (8 on an 8-GPU box)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                         "--master-addr", "127.0.0.1", "--master-port", "29533",
                         str(ROOT / "tests" / "multigpu_worker.py")], capture_output=True, text=True, timeout=600)
