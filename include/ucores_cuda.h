@@ -42,7 +42,10 @@ enum {
   UCG_ERR_NODEV = -3,    /* no CUDA device, or not compute capability 10.x */
   UCG_ERR_LENGTH = -4,   /* element lengths differ (reference LengthMismatch, errors.hpp:112) */
   UCG_ERR_EMPTY = -5,    /* reduce over zero elements (reference EmptyDataset, errors.hpp:80) */
-  UCG_ERR_NCCL = -6      /* collective failure */
+  UCG_ERR_NCCL = -6,     /* collective failure */
+  UCG_ERR_PEER = -7      /* a sharded exchange timed out in an earlier launch: a peer never
+                            published (that launch wrote NaN / -1 and kept its epoch); every
+                            call on the exchange fails until ucg_xchg_reset */
 };
 
 /* reduce operators: the combine of the binary kernels sum2 / max2 / isum2 */
@@ -177,6 +180,13 @@ uint64_t ucg_xchg_handle_bytes(void);
 int ucg_xchg_export(const ucg_xchg* x, void* handle_out);
 int ucg_xchg_open(ucg_xchg* x, const void* all_handles);
 int ucg_xchg_error(const ucg_xchg* x, int* err_out); /* 1 if a peer never arrived (synchronous) */
+/* The same error word read without synchronizing (it is host-mapped: the
+ * value of every launch that has completed so far). */
+int ucg_xchg_poll(const ucg_xchg* x, int* err_out);
+/* Recovery after UCG_ERR_PEER, called by EVERY rank between two barriers,
+ * with no exchange launch in flight: clears the error word, the epoch and
+ * this rank's region (its slots and flags). */
+int ucg_xchg_reset(ucg_xchg* x);
 int ucg_xchg_destroy(ucg_xchg* x);
 
 /* mapCLPartition(psum|pmax) + reduceCL stage 2 in ONE launch: the kernel

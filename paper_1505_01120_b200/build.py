@@ -50,10 +50,6 @@ def json_include() -> Path:
     return _site() / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
 
 
-def nccl_dir() -> Path:
-    return _site() / "nvidia" / "nccl"
-
-
 def _stale(target: Path, deps: list[Path]) -> bool:
     if not target.exists():
         return True
@@ -102,13 +98,11 @@ def build_engine(force: bool = False, verbose: bool = False) -> Path | None:
     deps = srcs + list((HOST / "ucores_b200").glob("*.hpp")) + [cuda_lib] + list(INCLUDE.glob("*.h"))
     if not (force or _stale(out, deps)):
         return out
-    nd = nccl_dir()
     cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-pthread", "-ffp-contract=off",
            "-I", str(REF_INC), "-I", str(json_include()), "-I", str(INCLUDE), "-I", str(HOST),
-           "-I", "/usr/local/cuda/include", "-I", str(nd / "include"),
+           "-I", "/usr/local/cuda/include",
            "-o", str(out)] + [str(s) for s in srcs] + [
            "-L", str(LIB), "-lucores_cuda", "-Wl,-rpath,$ORIGIN",
-           str(nd / "lib" / "libnccl.so.2"), "-Wl,-rpath," + str(nd / "lib"),
            "-L", "/usr/local/cuda/lib64", "-lcudart"]
     _run(cmd, verbose)
     return out
@@ -125,13 +119,11 @@ def build_tests(force: bool = False, verbose: bool = False) -> Path | None:
     if not (force or _stale(out, deps)):
         return out
     out.parent.mkdir(parents=True, exist_ok=True)
-    nd = nccl_dir()
     cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-ffp-contract=off",
            "-I", str(REF_INC), "-I", str(json_include()), "-I", str(INCLUDE), "-I", str(HOST),
-           "-I", "/usr/local/cuda/include", "-I", str(nd / "include"),
+           "-I", "/usr/local/cuda/include",
            "-o", str(out), str(src),
            "-L", str(LIB), "-lucores_cuda", "-Wl,-rpath," + str(LIB),
-           str(nd / "lib" / "libnccl.so.2"), "-Wl,-rpath," + str(nd / "lib"),
            "-L", "/usr/local/cuda/lib64", "-lcudart"]
     _run(cmd, verbose)
     return out

@@ -12,12 +12,12 @@ import os
 from pathlib import Path
 from typing import Sequence
 
-from .errors import DeviceUnavailable, EmptyDataset, KernelPanic, LengthMismatch
+from .errors import DeviceUnavailable, EmptyDataset, KernelPanic, LengthMismatch, PeerExchangeError
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libucores_cuda.so"
 
-OK, ERR_CUDA, ERR_ARG, ERR_NODEV, ERR_LENGTH, ERR_EMPTY, ERR_NCCL = 0, -1, -2, -3, -4, -5, -6
+OK, ERR_CUDA, ERR_ARG, ERR_NODEV, ERR_LENGTH, ERR_EMPTY, ERR_NCCL, ERR_PEER = 0, -1, -2, -3, -4, -5, -6, -7
 OP_SUM, OP_MAX = 0, 1
 OPS = {"sum": OP_SUM, "max": OP_MAX}
 
@@ -76,6 +76,8 @@ SIGNATURES: dict[str, tuple] = {
     "ucg_xchg_export": (i32, [vp, vp]),
     "ucg_xchg_open": (i32, [vp, vp]),
     "ucg_xchg_error": (i32, [vp, P(C.c_int)]),
+    "ucg_xchg_poll": (i32, [vp, P(C.c_int)]),
+    "ucg_xchg_reset": (i32, [vp]),
     "ucg_xchg_destroy": (i32, [vp]),
     "ucg_segment_reduce_cl_f32": (i32, [vp, vp, vp, f32, f32, C.c_int, vp, vp, vp, vp, vp]),
     "ucg_reduce_cl_f32": (i32, [vp, u64, u64, P(u64), u64, C.c_int, vp, vp]),
@@ -127,6 +129,8 @@ def check(rc: int, what: str = "run") -> None:
         raise LengthMismatch(msg)
     if rc == ERR_EMPTY:
         raise EmptyDataset(msg)
+    if rc == ERR_PEER:
+        raise PeerExchangeError(what, msg)
     raise KernelPanic(what, msg)
 
 
@@ -179,6 +183,8 @@ class SegTab:
 
     def __init__(self, begins: Sequence[int], lens: Sequence[int]):
         self.nseg = len(begins)
+        # the furthest float any segment touches: x / y must cover it
+        self.max_end = max((int(b) + int(n) for b, n in zip(begins, lens)), default=0)
         h = vp()
         call("ucg_segtab_create", u64_array(begins), u64_array(lens), self.nseg, C.byref(h), phase="map_parameters")
         self.handle = h.value

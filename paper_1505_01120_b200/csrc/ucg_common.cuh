@@ -16,6 +16,8 @@
 #error "libucores_cuda targets sm_100a only"
 #endif
 
+struct ucg_xchg;
+
 namespace ucg {
 
 // ---- error state ------------------------------------------------------------
@@ -23,6 +25,7 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 int check_device();  // UCG_OK when the current device is compute capability 10.x
+int xchg_guard(const ::ucg_xchg* x);  // UCG_ERR_PEER once a peer wait has timed out
 int sm_count();      // SMs of the current device (cached per device)
 extern std::atomic<uint64_t> g_launches;
 
@@ -139,7 +142,9 @@ struct ucg_xchg {
                             // overwrites values a peer may still be reading)
   uint64_t* d_peers;        // [world] device addresses of every rank's region (mapped)
   uint8_t** peer_ptrs;      // host copy (opened IPC handles, own region at [rank])
-  uint32_t* d_err;
+  uint32_t* h_err;          // error word in mapped pinned host memory: kernels store 1 on a
+  uint32_t* d_err;          // peer timeout (d_err = its device alias); entry points read h_err
+                            // without a sync and refuse to launch while it is set
   uint32_t* d_epoch;        // exchanges completed by this rank (advanced on the device, so
                             // sharded steps can be replayed from CUDA graphs)
   bool opened;

@@ -105,17 +105,27 @@ __device__ void pi_exchange(const PiXchg& x, unsigned long long* total) {
     st_release_sys_u32(reinterpret_cast<uint32_t*>(x.peers[r] + x.flags_offset) + x.rank, epoch);
   }
   const uint32_t* flags = reinterpret_cast<const uint32_t*>(x.peers[x.rank] + x.flags_offset);
+  bool timed_out = false;
   for (int r = lane; r < x.world; r += 32) {
     const uint64_t t0 = global_ns();
     while (int32_t(ld_acquire_sys_u32(flags + r) - epoch) < 0) {
       __nanosleep(64);
       if (global_ns() - t0 > kPeerWaitNs) {  // a peer never arrived
-        atomicExch(x.err, 1u);
+        timed_out = true;
         break;
       }
     }
   }
-  __syncwarp();
+  if (__any_sync(0xffffffffu, timed_out)) {
+    // no plausible total from stale slots: -1, the epoch unchanged, and the
+    // host-mapped error word raised (later calls fail with UCG_ERR_PEER)
+    if (lane == 0) {
+      *total = ~0ull;
+      *reinterpret_cast<volatile uint32_t*>(x.err) = 1u;
+      __threadfence_system();
+    }
+    return;
+  }
   if (lane == 0) {
     const volatile unsigned long long* slots = reinterpret_cast<const unsigned long long*>(x.peers[x.rank]);
     unsigned long long sum = 0;
@@ -202,6 +212,7 @@ int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, i
   if (xg) {
     if (!total_out) return fail(UCG_ERR_ARG, "the sharded pi total needs total_out");
     if (!xg->opened) return fail(UCG_ERR_ARG, "exchange context not opened");
+    if (int rc = xchg_guard(xg)) return rc;
     if (xg->p_total < 2ull * uint64_t(xg->world)) return fail(UCG_ERR_ARG, "pi exchange needs 2 slots per rank");
     int dev = -1;
     UCG_CUDA(cudaGetDevice(&dev));

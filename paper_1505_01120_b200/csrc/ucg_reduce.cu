@@ -285,7 +285,7 @@ struct FinishArgs {
   const uint64_t* peers;      // [world] region base addresses (this rank's own at [rank])
   uint64_t flags_offset;      // byte offset of the [world] epoch flags inside a region
   uint32_t* epoch;            // [1] exchanges completed (device counter; this one advances it)
-  uint32_t* err;              // set to 1 when a wait times out
+  uint32_t* err;              // host-mapped error word: set to 1 when a peer wait times out
   int warp_mode;              // one warp (not one CTA) per segment
   uint32_t finishers;         // fused tail: finisher CTAs (0 = min(G, nseg))
   int flag_exchange;          // sharded: 1 = data stores + fence + epoch flags (A/B), 0 = one
@@ -411,6 +411,19 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
   }
 }
 
+// A peer never published within kPeerWaitNs: the result is NaN (never a
+// plausible value reduced from stale slots), the epoch stays where it was,
+// and the exchange's error word — host-mapped, so every later C entry point
+// on this exchange sees it without a device sync and fails with
+// UCG_ERR_PEER until ucg_xchg_reset — is raised.
+__device__ __noinline__ void peer_timeout(const FinishArgs& p) {
+  if (threadIdx.x == 0) {
+    *p.result = __int_as_float(0x7fc00000);
+    *reinterpret_cast<volatile uint32_t*>(p.err) = 1u;
+    __threadfence_system();
+  }
+}
+
 // Called by all F finisher CTAs after their segments are written. The last
 // one to arrive resets the counters and runs reduce_cl stage 2: on one GPU
 // directly over the partition values; sharded, it first stores this rank's
@@ -460,6 +473,7 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
   const float* vals = p.out;
   uint64_t nvals = p.nseg;
   uint32_t epoch = 0;
+  bool timed_out = false;
   if (p.world > 1 && !p.flag_exchange) {
     // Each value travels with its epoch in ONE 64-bit store to every peer's
     // slot (single-copy atomic), so a reader that sees the epoch has the
@@ -483,14 +497,14 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
         uint32_t spins = 0;
         while (uint32_t((v = ld_relaxed_sys_u64(mine + i)) >> 32) != epoch) {
           if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) {  // a peer never arrived
-            atomicExch(p.err, 1u);
+            timed_out = true;
             break;
           }
         }
       }
       gathered[i] = __uint_as_float(uint32_t(v));
     }
-    __syncthreads();
+    if (__syncthreads_or(timed_out)) return peer_timeout(p);
     vals = gathered;
     nvals = p.p_total;
   } else if (p.world > 1) {
@@ -511,12 +525,12 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
       while (int32_t(ld_acquire_sys(mine) - epoch) < 0) {
         __nanosleep(64);
         if (global_ns() - t0 > kPeerWaitNs) {  // a peer never arrived
-          atomicExch(p.err, 1u);
+          timed_out = true;
           break;
         }
       }
     }
-    __syncthreads();
+    if (__syncthreads_or(timed_out)) return peer_timeout(p);
     vals = reinterpret_cast<const float*>(p.peers[p.rank]) + buf;
     nvals = p.p_total;
   }
@@ -619,9 +633,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
     uint64_t spins = 0;
     while (ld_acquire_gpu(p.fin.done) < G) {
       __nanosleep(32);
-      if (++spins > (1ull << 25)) {  // cannot happen under a cooperative launch
-        if (p.fin.err) atomicExch(p.fin.err, 2u);
-        break;
+      if (++spins > (1ull << 25)) {  // cannot happen under a cooperative launch:
+        __trap();                    // never reduce item roots that are not all written
       }
     }
   }
@@ -769,7 +782,7 @@ struct F32MaxE {
 //  stage 2 (engine.hpp:172-190): one thread per lane, the pairing tree over
 //    the partition partials in partition order (binary-counter stack of
 //    aligned subtrees, folded right to left).
-constexpr int kMaxParts = 4096;  // stage-2 stack depth 13
+constexpr int kStage2Depth = 64;  // binary-counter stack: one slot per bit of the partition count
 
 template <class T, class Op>
 __global__ void __launch_bounds__(256) k_fold_warp(const T* const* __restrict__ elems,
@@ -820,7 +833,7 @@ __global__ void __launch_bounds__(128) k_stage2(const T* __restrict__ partials, 
                                                 T* __restrict__ out) {
   const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= len) return;
-  T stk[13];  // nonempty <= 4096 -> depth <= 12
+  T stk[kStage2Depth];  // slot l holds an aligned subtree of 2^l partials (no partition limit)
   for (uint64_t k = 0; k < nonempty; ++k) {
     T acc = partials[k * len + j];
     int lvl = 0;
@@ -834,7 +847,7 @@ __global__ void __launch_bounds__(128) k_stage2(const T* __restrict__ partials, 
   bool have = false;
   T acc{};
 #pragma unroll 1
-  for (int lvl = 0; lvl < 13; ++lvl) {
+  for (int lvl = 0; lvl < kStage2Depth; ++lvl) {
     if ((nonempty >> lvl) & 1) {
       acc = have ? Op::apply(stk[lvl], acc) : stk[lvl];
       have = true;
@@ -1001,7 +1014,6 @@ int reduce_cl(const T* const* elem_ptrs, uint64_t count, uint64_t len, const uin
   if (total != count) return fail(UCG_ERR_ARG, "part_counts do not sum to count");
   if (count == 0) return fail(UCG_ERR_EMPTY, "reduce_cl needs at least one element");
   const uint64_t nonempty = first.size() - 1;
-  if (nonempty > kMaxParts) return fail(UCG_ERR_ARG, "more than 4096 non-empty partitions");
   if (len == 0) return UCG_OK;
   uint64_t* d_first = nullptr;
   T* d_part = nullptr;
@@ -1120,6 +1132,9 @@ int ucg_segment_reduce_cl_f32(const float* x, float* y, const ucg_segtab* t, flo
   if (t->nseg && (!partials || (t->nitems && (!x || !scratch)))) return fail(UCG_ERR_ARG, "null argument");
   if (t->nitems && (!aligned16(x) || (y && !aligned16(y)))) return fail(UCG_ERR_ARG, "x/y must be 16-byte aligned");
   if (xchg && (!xchg->opened || xchg->nloc != t->nseg)) return fail(UCG_ERR_ARG, "exchange not opened for this shard");
+  if (xchg) {
+    if (int rc = xchg_guard(xchg)) return rc;
+  }
   if (op == UCG_OP_SUM) return segment_reduce<OpSum>(x, y, t, a, b, scratch, partials, result, xchg, as_stream(stream));
   if (op == UCG_OP_MAX) return segment_reduce<OpMax>(x, y, t, a, b, scratch, partials, result, xchg, as_stream(stream));
   return fail(UCG_ERR_ARG, "unknown op");
@@ -1129,6 +1144,7 @@ int ucg_reduce_cl_xchg_f32(float* partials, uint64_t nloc, int op, ucg_xchg* xch
   if (int rc = check_device()) return rc;
   if (!xchg || !result || (nloc && !partials)) return fail(UCG_ERR_ARG, "null argument");
   if (!xchg->opened || xchg->nloc != nloc) return fail(UCG_ERR_ARG, "exchange not opened for this shard");
+  if (int rc = xchg_guard(xchg)) return rc;
   int dev = -1;
   UCG_CUDA(cudaGetDevice(&dev));
   if (dev != xchg->device) return fail(UCG_ERR_ARG, "exchange context belongs to another device");

@@ -62,6 +62,14 @@ const DevCache* dev_cache(int* dev_out) {
 }
 }  // namespace
 
+// Entry-point guard of every launch on an exchange (reads the host-mapped
+// error word: no device sync).
+int xchg_guard(const ucg_xchg* x) {
+  if (*reinterpret_cast<volatile uint32_t*>(x->h_err))
+    return fail(UCG_ERR_PEER, "peer exchange timed out in an earlier launch (ucg_xchg_reset on every rank to recover)");
+  return UCG_OK;
+}
+
 int check_device() {
   int dev = -1;
   const DevCache* c = dev_cache(&dev);
@@ -408,16 +416,19 @@ int ucg_xchg_create(int world, int rank, uint64_t nloc, uint64_t part_offset, ui
   x->peer_ptrs = new uint8_t*[world]();
   cudaError_t e;
   if ((e = cudaMalloc(&x->region, x->region_bytes)) != cudaSuccess || (e = cudaMemset(x->region, 0, x->region_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&x->d_peers, world * 8)) != cudaSuccess || (e = cudaMalloc(&x->d_err, 8)) != cudaSuccess ||
-      (e = cudaMemset(x->d_err, 0, 8)) != cudaSuccess) {
+      (e = cudaMalloc(&x->d_peers, world * 8)) != cudaSuccess || (e = cudaMalloc(&x->d_epoch, 4)) != cudaSuccess ||
+      (e = cudaMemset(x->d_epoch, 0, 4)) != cudaSuccess ||
+      (e = cudaHostAlloc(&x->h_err, 4, cudaHostAllocMapped)) != cudaSuccess ||
+      (e = cudaHostGetDevicePointer(&x->d_err, x->h_err, 0)) != cudaSuccess) {
     cudaFree(x->region);
     cudaFree(x->d_peers);
-    cudaFree(x->d_err);
+    cudaFree(x->d_epoch);
+    if (x->h_err) cudaFreeHost(x->h_err);
     delete[] x->peer_ptrs;
     delete x;
     return cuda_fail(e, "ucg_xchg_create");
   }
-  x->d_epoch = x->d_err + 1;  // the second word of the 8-byte allocation
+  *x->h_err = 0;
   *out = x;
   return UCG_OK;
 }
@@ -454,9 +465,34 @@ int ucg_xchg_open(ucg_xchg* x, const void* all_handles) {
 
 int ucg_xchg_error(const ucg_xchg* x, int* err_out) {
   if (!x || !err_out) return fail(UCG_ERR_ARG, "null argument");
-  uint32_t e = 0;
-  UCG_CUDA(cudaMemcpy(&e, x->d_err, 4, cudaMemcpyDeviceToHost));
-  *err_out = int(e);
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != x->device) UCG_CUDA(cudaSetDevice(x->device));
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (cur >= 0 && cur != x->device) cudaSetDevice(cur);
+  UCG_CUDA(e);
+  *err_out = int(*reinterpret_cast<volatile uint32_t*>(x->h_err));
+  return UCG_OK;
+}
+
+int ucg_xchg_poll(const ucg_xchg* x, int* err_out) {
+  if (!x || !err_out) return fail(UCG_ERR_ARG, "null argument");
+  *err_out = int(*reinterpret_cast<volatile uint32_t*>(x->h_err));
+  return UCG_OK;
+}
+
+int ucg_xchg_reset(ucg_xchg* x) {
+  if (!x) return fail(UCG_ERR_ARG, "null argument");
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != x->device) UCG_CUDA(cudaSetDevice(x->device));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemset(x->region, 0, x->region_bytes);
+  if (e == cudaSuccess) e = cudaMemset(x->d_epoch, 0, 4);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (cur >= 0 && cur != x->device) cudaSetDevice(cur);
+  UCG_CUDA(e);
+  *reinterpret_cast<volatile uint32_t*>(x->h_err) = 0;
   return UCG_OK;
 }
 
@@ -466,7 +502,8 @@ int ucg_xchg_destroy(ucg_xchg* x) {
     if (x->peer_ptrs[r] && r != x->rank) cudaIpcCloseMemHandle(x->peer_ptrs[r]);
   cudaFree(x->region);
   cudaFree(x->d_peers);
-  cudaFree(x->d_err);
+  cudaFree(x->d_epoch);
+  cudaFreeHost(x->h_err);
   delete[] x->peer_ptrs;
   delete x;
   return UCG_OK;

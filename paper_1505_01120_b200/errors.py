@@ -42,6 +42,13 @@ class KernelPanic(Error):
         self.phase = phase
 
 
+class PeerExchangeError(KernelPanic):
+    """A sharded reduce_cl's NVLink exchange timed out: a peer rank never
+    published its partials (the affected launch wrote NaN / -1, not a
+    plausible value). Every later launch on that exchange raises this until
+    all ranks call MapReducePipeline.reset_exchange()."""
+
+
 class EmptyDataset(Error):
     """errors.hpp:80-83: reduce_cl over zero elements."""
 

@@ -38,6 +38,29 @@ def _dtype(t, want, name: str) -> None:
         raise TypeError(f"{name} must be {want}, got {t.dtype}")
 
 
+def _f32(*named) -> None:
+    import torch
+
+    for name, t in named:
+        _dtype(t, torch.float32, name)
+
+
+def _at_least(t, n: int, name: str) -> None:
+    if t is not None and t.numel() < n:
+        raise ValueError(f"{name} holds {t.numel()} elements, needs >= {n}")
+
+
+def _check_segments(segtab: capi.SegTab, x, y, scratch, partials) -> None:
+    """Every buffer a segment-table launch indexes covers the extents the
+    table implies: x / y its furthest segment end, scratch its item roots,
+    partials one value per segment."""
+    _f32(("x", x), ("y", y), ("scratch", scratch), ("partials", partials))
+    _at_least(x, segtab.max_end, "x")
+    _at_least(y, segtab.max_end, "y")
+    _at_least(scratch, segtab.scratch_floats, "scratch")
+    _at_least(partials, segtab.nseg, "partials")
+
+
 def fill_uniform_(out, seed: int, first: int = 0, stream=None):
     """Synthetic U[0,1) input: out[i] = (mix64(seed + (first+i+1)*GAMMA) >> 40) * 2^-24."""
     _require_cuda(out)
@@ -71,6 +94,10 @@ def elementwise2(a, b, c, op: str = "sum", stream=None):
         raise capi.LengthMismatch("vector lengths differ")
     import torch
 
+    if not (a.dtype == b.dtype == c.dtype) or a.dtype not in (torch.float32, torch.int64):
+        raise TypeError("a, b, c must all be float32 or all int64")
+    _at_least(c, a.numel(), "c")
+
     if a.dtype == torch.int64:
         call("ucg_elementwise2_i64", ptr(a), ptr(b), ptr(c), a.numel(), stream_handle(stream))
     else:
@@ -81,6 +108,7 @@ def elementwise2(a, b, c, op: str = "sum", stream=None):
 def segment_reduce(x, segtab: capi.SegTab, op: str, scratch, out, stream=None):
     """mapCLPartition psum/pmax over every segment (engine.hpp:89-114)."""
     _require_cuda(x, scratch, out)
+    _check_segments(segtab, x, None, scratch, out)
     call("ucg_segment_reduce_f32", ptr(x), segtab.handle, capi.OPS[op], ptr(scratch), ptr(out),
          stream_handle(stream))
     return out
@@ -89,6 +117,7 @@ def segment_reduce(x, segtab: capi.SegTab, op: str, scratch, out, stream=None):
 def map_affine_segment_reduce(x, y, segtab: capi.SegTab, a: float, b: float, op: str, scratch, out, stream=None):
     """Fused mapCL(axpb) -> mapCLPartition(psum|pmax): y written, partials reduced."""
     _require_cuda(x, y, scratch, out)
+    _check_segments(segtab, x, y, scratch, out)
     call("ucg_map_affine_segment_reduce_f32", ptr(x), ptr(y), segtab.handle, a, b, capi.OPS[op], ptr(scratch),
          ptr(out), stream_handle(stream))
     return out
@@ -98,7 +127,10 @@ def segment_reduce_cl(x, y, segtab: capi.SegTab, a: float, b: float, op: str, sc
                       stream=None):
     """map_cl(axpb) (when y is given) -> map_cl_partition(p<op>) -> reduce_cl(<op>2) in one launch;
     xchg (a ucg_xchg handle) makes the last stage a fused cross-GPU exchange."""
-    _require_cuda(x, scratch, partials, result)
+    _require_cuda(x, y, scratch, partials, result)
+    _check_segments(segtab, x, y, scratch, partials)
+    _f32(("result", result))
+    _at_least(result, 1, "result")
     call("ucg_segment_reduce_cl_f32", ptr(x), ptr(y), segtab.handle, a, b, capi.OPS[op], ptr(scratch), ptr(partials),
          xchg, ptr(result), stream_handle(stream))
     return result
@@ -107,6 +139,9 @@ def segment_reduce_cl(x, y, segtab: capi.SegTab, a: float, b: float, op: str, sc
 def tree_reduce(x, n: int, op: str, out, stream=None):
     """reduceCL stage 2 over n one-float partials (engine.hpp:172-190)."""
     _require_cuda(x, out)
+    _f32(("x", x), ("out", out))
+    _at_least(x, n, "x")
+    _at_least(out, 1, "out")
     call("ucg_tree_reduce_f32", ptr(x), n, capi.OPS[op], ptr(out), stream_handle(stream))
     return out
 
@@ -118,6 +153,14 @@ def reduce_cl_vectors(elem_ptrs, count: int, length: int, part_counts: Sequence[
     elem_ptrs: int64 CUDA tensor holding the device addresses of the elements.
     """
     _require_cuda(elem_ptrs, out)
+    import torch
+
+    _dtype(elem_ptrs, torch.int64, "elem_ptrs")
+    _dtype(out, torch.int64 if dtype == "i64" else torch.float32, "out")
+    _at_least(elem_ptrs, count, "elem_ptrs")
+    _at_least(out, length, "out")
+    if sum(part_counts) != count:
+        raise ValueError("part_counts do not sum to count")
     pc = u64_array(part_counts)
     if dtype == "i64":
         call("ucg_reduce_cl_i64", ptr(elem_ptrs), count, length, pc, len(part_counts), ptr(out),
@@ -135,6 +178,14 @@ def pi_hits(seeds: Sequence[int], samples: Sequence[int], hits_out, stream=None,
     per rank), total_out is the sum over all ranks, exchanged over NVLink by
     the same kernel."""
     _require_cuda(hits_out)
+    import torch
+
+    if len(seeds) != len(samples):
+        raise ValueError("one sample count per task seed")
+    _dtype(hits_out, torch.int64, "hits_out")
+    _dtype(total_out, torch.int64, "total_out")
+    _at_least(hits_out, len(seeds), "hits_out")
+    _at_least(total_out, 1, "total_out")
     if xchg is not None:
         _require_cuda(total_out)
         call("ucg_pi_hits_total_xchg", u64_array(seeds), u64_array(samples), len(seeds), ptr(hits_out),
@@ -152,6 +203,14 @@ def sobel_bands(inp, in_off: Sequence[int], out, out_off: Sequence[int], rows: S
                 stream=None):
     """mapCLPartition sobel over row bands (one launch for all bands)."""
     _require_cuda(inp, out)
+    import torch
+
+    _dtype(inp, torch.uint8, "inp")
+    _dtype(out, torch.uint8, "out")
+    if not (len(in_off) == len(out_off) == len(rows)):
+        raise ValueError("one input offset, output offset and row count per band")
+    _at_least(inp, max((o + (r + 2) * width for o, r in zip(in_off, rows)), default=0), "inp")
+    _at_least(out, max((o + r * width for o, r in zip(out_off, rows)), default=0), "out")
     call("ucg_sobel_bands_u8", ptr(inp), u64_array(in_off), ptr(out), u64_array(out_off), u64_array(rows),
          len(rows), width, stream_handle(stream))
     return out
@@ -160,12 +219,24 @@ def sobel_bands(inp, in_off: Sequence[int], out, out_off: Sequence[int], rows: S
 def word_start_flags(data, flags, stream=None):
     """wordcount run() over one chunk: 1 at every byte that starts a word."""
     _require_cuda(data, flags)
+    import torch
+
+    _dtype(data, torch.uint8, "data")
+    _dtype(flags, torch.uint8, "flags")
+    _at_least(flags, data.numel(), "flags")
     call("ucg_word_start_flags", ptr(data), data.numel(), ptr(flags), stream_handle(stream))
     return flags
 
 
+def _check_gemm(A, B, Cm, n: int) -> None:
+    _f32(("A", A), ("B", B), ("C", Cm))
+    for name, t in (("A", A), ("B", B), ("C", Cm)):
+        _at_least(t, n * n, name)
+
+
 def gemm_tf32(A, B, Cm, n: int, stream=None):
     _require_cuda(A, B, Cm)
+    _check_gemm(A, B, Cm, n)
     call("ucg_gemm_tf32", ptr(A), ptr(B), ptr(Cm), n, stream_handle(stream))
     return Cm
 
@@ -173,5 +244,6 @@ def gemm_tf32(A, B, Cm, n: int, stream=None):
 def gemm_f32(A, B, Cm, n: int, stream=None):
     """fp32-faithful C = A @ B on the tensor cores (3xTF32 split, ucg_gemm_f32)."""
     _require_cuda(A, B, Cm)
+    _check_gemm(A, B, Cm, n)
     call("ucg_gemm_f32", ptr(A), ptr(B), ptr(Cm), n, stream_handle(stream))
     return Cm

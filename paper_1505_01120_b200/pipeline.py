@@ -260,8 +260,32 @@ class MapReducePipeline:
                         self.step()
             torch.cuda.current_stream().wait_stream(side)
             graphs[steps] = g
+        self._poll_exchange()  # replays bypass the C entry point's error guard
         graphs[steps].replay()
         return self.result
+
+    def _poll_exchange(self) -> None:
+        """Raise PeerExchangeError if an earlier exchange timed out (reads the
+        host-mapped error word: no device sync)."""
+        import ctypes as C
+
+        if getattr(self, "xchg", None) is None:
+            return
+        e = C.c_int(0)
+        capi.call("ucg_xchg_poll", self.xchg, C.byref(e))
+        if e.value:
+            capi.check(capi.ERR_PEER, "run")
+
+    def reset_exchange(self) -> None:
+        """Recovery after PeerExchangeError: every rank calls this (it
+        barriers on the process group) — error word, epoch and region cleared."""
+        import torch.distributed as dist
+
+        if getattr(self, "xchg", None) is None:
+            return
+        dist.barrier(group=self.group)
+        capi.call("ucg_xchg_reset", self.xchg)
+        dist.barrier(group=self.group)
 
     def exchange_error(self) -> int:
         """1 if a peer never published its partials (checked synchronously)."""
