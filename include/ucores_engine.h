@@ -52,6 +52,15 @@ int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts,
                      int gpus, int mode, float* y_out, float* partials_out, float* result_out,
                      double* seconds_out);
 
+/* ucd_pipeline_f32 (BATCHED mode) with a time breakdown, for profiling the
+ * drop-in: out8 = {map_cl seconds, of which inside the driver's run_wave,
+ * map_cl_partition seconds, of which run_wave, reduce_cl seconds, of which
+ * run_wave, the whole chain, the result's fp32 bit pattern}. Time outside
+ * run_wave is the reference Engine's own work (task input copies,
+ * Element::concat, result assembly). */
+int ucd_pipeline_breakdown_f32(const float* x, const uint64_t* part_lens, uint64_t nparts, float a, float b, int op,
+                               int gpus, double* out8);
+
 /* The C1 literal form: n one-float elements x[i] in nparts
  * partitions (create_dataset, ceiling-first), then the same chain as
  * ucd_pipeline_f32. map_cl is one task per element in the reference; the GPU

@@ -28,6 +28,9 @@ def load() -> C.CDLL:
         L.ucd_pipeline_f32.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64, C.c_float, C.c_float, C.c_int,
                                        C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_float),
                                        C.POINTER(C.c_double)]
+        L.ucd_pipeline_breakdown_f32.restype = C.c_int
+        L.ucd_pipeline_breakdown_f32.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64, C.c_float, C.c_float,
+                                                 C.c_int, C.c_int, C.c_void_p]
         L.ucd_literal_f32.restype = C.c_int
         L.ucd_literal_f32.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_float, C.c_float, C.c_int, C.c_int,
                                       C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_double)]
@@ -56,6 +59,22 @@ def pipeline_f32(x: np.ndarray, part_lens, a: float = 2.0, b: float = 1.0, op: s
                                    y.ctypes.data if want_y else None, partials.ctypes.data, C.byref(res),
                                    C.byref(sec)))
     return y, partials, np.float32(res.value), sec.value
+
+
+def pipeline_breakdown_f32(x: np.ndarray, part_lens, a: float = 2.0, b: float = 1.0, op: str = "sum",
+                           gpus: int = -1) -> dict:
+    """Seconds of each reference Engine call of the C2 chain through seam A,
+    split into the driver's run_wave time and the Engine's own work."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.zeros(8, np.float64)
+    _check(load().ucd_pipeline_breakdown_f32(x.ctypes.data, capi.u64_array(part_lens), len(part_lens), a, b,
+                                             capi.OPS[op], gpus, out.ctypes.data))
+    keys = ["map_cl_s", "map_cl_wave_s", "map_cl_partition_s", "map_cl_partition_wave_s", "reduce_cl_s",
+            "reduce_cl_wave_s", "total_s"]
+    d = {k: float(v) for k, v in zip(keys, out[:7])}
+    d["engine_own_s"] = d["total_s"] - d["map_cl_wave_s"] - d["map_cl_partition_wave_s"] - d["reduce_cl_wave_s"]
+    d["result_bits"] = "%08x" % int(out[7])
+    return d
 
 
 def literal_f32(x: np.ndarray, parts: int, a: float = 2.0, b: float = 1.0, op: str = "sum", gpus: int = -1,

@@ -127,6 +127,71 @@ int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts,
   });
 }
 
+int ucd_pipeline_breakdown_f32(const float* x, const uint64_t* part_lens, uint64_t nparts, float a, float b, int op,
+                               int gpus, double* out8) {
+  return guarded([&] {
+    using namespace ucores;
+    using namespace ucores_b200;
+    KernelRegistry reg;
+    DeviceOpRegistry ops;
+    WorkloadParams p;
+    p.a = a;
+    p.b = b;
+    register_workload(reg, ops, p);
+    const std::string pk = op == 1 ? "pmax" : "psum", rk = op == 1 ? "max2" : "sum2";
+    GpuClusterDriver::Options opt;
+    opt.max_gpus = gpus;
+    GpuClusterDriver inner(reg, ops, opt);
+    // times the driver's run_wave inside each Engine call: the rest of the
+    // call is the reference Engine's own work (task input copies, concat,
+    // result assembly)
+    struct Timed : ClusterDriver {
+      GpuClusterDriver* d;
+      double wave_s = 0;
+      std::uint64_t new_job_id() override { return d->new_job_id(); }
+      std::vector<TaskResult> run_wave(std::vector<Task> tasks, int max_retries) override {
+        auto t0 = std::chrono::steady_clock::now();
+        auto r = d->run_wave(std::move(tasks), max_retries);
+        wave_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return r;
+      }
+    } drv;
+    drv.d = &inner;
+    Engine eng(drv, reg);
+    std::vector<Partition> parts(nparts);
+    std::uint64_t off = 0;
+    for (std::uint64_t q = 0; q < nparts; ++q) {
+      parts[q].elements.push_back(Element::f32(std::vector<float>(x + off, x + off + part_lens[q])));
+      off += part_lens[q];
+    }
+    Dataset d(std::move(parts));
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    auto t0 = now();
+    Dataset y = eng.map_cl(d, "axpb");
+    auto t1 = now();
+    const double w1 = drv.wave_s;
+    Dataset ps = eng.map_cl_partition(y, pk);
+    auto t2 = now();
+    const double w2 = drv.wave_s - w1;
+    Element r = eng.reduce_cl(ps, rk);
+    auto t3 = now();
+    const double w3 = drv.wave_s - w1 - w2;
+    // [map_cl total, its waves, map_cl_partition total, its waves, reduce_cl
+    //  total, its waves, the whole chain, result bits]
+    out8[0] = sec(t0, t1);
+    out8[1] = w1;
+    out8[2] = sec(t1, t2);
+    out8[3] = w2;
+    out8[4] = sec(t2, t3);
+    out8[5] = w3;
+    out8[6] = sec(t0, t3);
+    std::uint32_t bits;
+    std::memcpy(&bits, r.as_f32().data(), 4);
+    out8[7] = double(bits);
+  });
+}
+
 int ucd_literal_f32(const float* x, uint64_t n, uint64_t nparts, float a, float b, int op, int gpus, int mode,
                     float* result_out, double* seconds_out) {
   return guarded([&] {

@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <list>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -184,92 +185,15 @@ class DeviceDataset {
   std::vector<std::shared_ptr<GpuAlloc>> bufs_;  // one per engine GPU (may be null)
 };
 
-/// Persistent host threads for the staging copies (a pageable Element payload
-/// into a pinned staging half): one parallel memcpy per call, split into
-/// equal slices; no thread creation on the upload path.
-class CopyPool {
- public:
-  explicit CopyPool(unsigned n) {
-    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
-    n_ = n;
-  }
-  ~CopyPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : workers_) t.join();
-  }
-  void copy(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len) {
-    if (n_ <= 1 || len < (1u << 20)) {
-      std::memcpy(dst, src, len);
-      return;
-    }
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      dst_ = dst;
-      src_ = src;
-      len_ = len;
-      pending_ = n_ - 1;
-      ++gen_;
-    }
-    cv_.notify_all();
-    slice(0, dst, src, len);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [&] { return pending_ == 0; });
-  }
-
- private:
-  void slice(unsigned i, std::uint8_t* dst, const std::uint8_t* src, std::uint64_t len) const {
-    const std::uint64_t per = (len + n_ - 1) / n_;
-    const std::uint64_t b = std::min(len, i * per), e = std::min(len, b + per);
-    if (b < e) std::memcpy(dst + b, src + b, e - b);
-  }
-  void loop(unsigned i) {
-    std::uint64_t seen = 0;
-    for (;;) {
-      std::uint8_t* dst;
-      const std::uint8_t* src;
-      std::uint64_t len;
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
-        dst = dst_;
-        src = src_;
-        len = len_;
-      }
-      slice(i, dst, src, len);
-      {
-        std::lock_guard<std::mutex> lk(mu_);
-        if (--pending_ == 0) done_cv_.notify_one();
-      }
-    }
-  }
-  std::vector<std::thread> workers_;
-  unsigned n_ = 1;
-  std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  bool stop_ = false;
-  std::uint64_t gen_ = 0;
-  unsigned pending_ = 0;
-  std::uint8_t* dst_ = nullptr;
-  const std::uint8_t* src_ = nullptr;
-  std::uint64_t len_ = 0;
-};
-
 class DeviceEngine {
  public:
   explicit DeviceEngine(WorkloadParams params = {}, int max_gpus = -1) : params_(params) {
     for (auto& g : open_gpus(max_gpus)) gpus_.push_back(std::move(g));
-    // bring-up: the upload path's pinned staging halves (2 x 64 MB per GPU)
-    // and copy threads exist before the first upload, as a worker's
-    // resources exist before its first task
-    staging_.resize(gpus_.size());
-    for (std::size_t g = 0; g < gpus_.size(); ++g) ensure_staging(g);
-    ensure_copy_pool();
+    // bring-up: each GPU's transfer pipeline (pinned slot rings, copy
+    // streams) and the host copy threads exist before the first upload, as a
+    // worker's resources exist before its first task
+    for (auto& g : gpus_) g->attached<HostPipe>();
+    work_pool();
   }
   std::size_t gpu_count() const { return gpus_.size(); }
 
@@ -291,23 +215,27 @@ class DeviceEngine {
       }
     }
     DeviceDataset out = allocate(std::move(parts));
-    for (std::size_t p = 0; p < out.parts_.size(); ++p) {
-      std::vector<std::pair<const std::uint8_t*, std::uint64_t>> pieces;
-      for (const ucores::Element& e : d.partitions()[p].elements)
-        pieces.emplace_back(static_cast<const std::uint8_t*>(host_bytes(e)), e.byte_size());
-      upload_partition(out.parts_[p].gpu, out.data(p), pieces);
-    }
-    sync_all();
-    return out;
-  }
-
-  ~DeviceEngine() {
-    for (Staging& s : staging_) {
-      for (int k = 0; k < 2; ++k) {
-        if (s.ev[k]) ucg_event_destroy(s.ev[k]);
-        if (s.buf[k]) ucg_host_free(s.buf[k]);
+    // every GPU's partitions through its pipe, the GPUs concurrently (one
+    // host thread each): a partition's elements land back to back, so its
+    // bytes are its concatenation; small elements share a pinned slot
+    run_per_gpu([&](std::size_t g) {
+      HostPipe& pipe = gpus_[g]->attached<HostPipe>();
+      for (std::size_t p = 0; p < out.parts_.size(); ++p) {
+        if (out.parts_[p].gpu != g) continue;
+        std::vector<std::span<const std::uint8_t>> pieces;
+        std::vector<std::uint64_t> off;
+        std::uint64_t at = 0;
+        for (const ucores::Element& e : d.partitions()[p].elements) {
+          pieces.emplace_back(static_cast<const std::uint8_t*>(host_bytes(e)), e.byte_size());
+          off.push_back(at);
+          at += e.byte_size();
+        }
+        pipe.upload_pieces(out.data(p), pieces, off);
       }
-    }
+      pipe.compute_after_upload();
+      pipe.drain();
+    });
+    return out;
   }
 
   /// HBM -> host Dataset (the lazy collect of SURVEY §8(f)1).
@@ -593,8 +521,14 @@ class DeviceEngine {
         check(ucg_segment_reduce_f32(base, tab, kernel == "pmax" ? UCG_OP_MAX : UCG_OP_SUM,
                                      reinterpret_cast<float*>(scratch->at(0)), reinterpret_cast<float*>(vals->at(0)),
                                      st));
-        for (std::size_t i = 0; i < units.size(); ++i)
-          check(ucg_memcpy_d2d(ob + ounits[i].in_off, vals->at(i * 4), 4, st));
+        // the values of one partition's units are contiguous on both sides:
+        // one copy per partition, not one per unit
+        for (std::size_t i = 0; i < units.size();) {
+          std::size_t j = i + 1;
+          while (j < units.size() && units[j].part == units[i].part) ++j;
+          check(ucg_memcpy_d2d(ob + ounits[i].in_off, vals->at(i * 4), (j - i) * 4, st));
+          i = j;
+        }
       } else if (kernel == "sobel") {
         std::vector<std::uint64_t> in_off, out_off, rows;
         for (std::size_t i = 0; i < units.size(); ++i) {
@@ -604,9 +538,14 @@ class DeviceEngine {
         }
         check(ucg_sobel_bands_u8(ib, in_off.data(), ob, out_off.data(), rows.data(), rows.size(), w, st));
       } else if (kernel == "pi") {
+        // {seed, samples} of one partition's units are contiguous: one copy each
         std::vector<std::int64_t> params(units.size() * 2);
-        for (std::size_t i = 0; i < units.size(); ++i)
-          check(ucg_memcpy_d2h(&params[2 * i], ib + units[i].in_off, 16, st));
+        for (std::size_t i = 0; i < units.size();) {
+          std::size_t j = i + 1;
+          while (j < units.size() && units[j].part == units[i].part) ++j;
+          check(ucg_memcpy_d2h(&params[2 * i], ib + units[i].in_off, (j - i) * 16, st));
+          i = j;
+        }
         check(ucg_stream_synchronize(st));
         std::vector<std::uint64_t> seeds(units.size()), samples(units.size());
         for (std::size_t i = 0; i < units.size(); ++i) {
@@ -617,11 +556,23 @@ class DeviceEngine {
         keep.push_back(hits);
         check(ucg_pi_hits(seeds.data(), samples.data(), units.size(), reinterpret_cast<std::int64_t*>(hits->at(0)),
                           st));
+        // outputs {hits, samples}: the hits come back once, the pairs go up
+        // once per partition
+        std::vector<std::int64_t> h(units.size()), pairs(2 * units.size());
+        check(ucg_memcpy_d2h(h.data(), hits->at(0), h.size() * 8, st));
+        check(ucg_stream_synchronize(st));
         for (std::size_t i = 0; i < units.size(); ++i) {
-          check(ucg_memcpy_d2d(ob + ounits[i].in_off, hits->at(i * 8), 8, st));
-          // pageable source: staged before the call returns, so `samples` may go
-          check(ucg_memcpy_h2d(ob + ounits[i].in_off + 8, &samples[i], 8, st));
+          pairs[2 * i] = h[i];
+          pairs[2 * i + 1] = static_cast<std::int64_t>(samples[i]);
         }
+        for (std::size_t i = 0; i < units.size();) {
+          std::size_t j = i + 1;
+          while (j < units.size() && units[j].part == units[i].part) ++j;
+          // pageable source: staged before the call returns
+          check(ucg_memcpy_h2d(ob + ounits[i].in_off, &pairs[2 * i], (j - i) * 16, st));
+          i = j;
+        }
+        check(ucg_stream_synchronize(st));
       } else {  // matmul
         for (std::size_t i = 0; i < units.size(); ++i) {
           const float* a = reinterpret_cast<const float*>(ib + units[i].in_off);
@@ -634,87 +585,25 @@ class DeviceEngine {
     return out;
   }
 
-  // -- upload path -------------------------------------------------------------------
-  // Element payloads live in pageable std::vectors. Large ones are copied by
-  // several host threads into a pinned double buffer per GPU while the copy
-  // engine drains the other half, so the upload runs near the PCIe rate
-  // instead of the driver's single-threaded pageable staging.
-  static constexpr std::uint64_t kStageBytes = 64ull << 20;
-  static constexpr std::uint64_t kDirectBytes = 4ull << 20;  // below this: one pageable copy
-  struct Staging {
-    void* buf[2] = {nullptr, nullptr};
-    void* ev[2] = {nullptr, nullptr};
-    bool busy[2] = {false, false};
-    int next = 0;
-  };
-
-  // A partition's element payloads, packed back to back (its device layout)
-  // through the staging halves: one DMA per filled half, so a partition of
-  // 2^18 one-float elements is one copy, not 2^18.
-  void upload_partition(std::size_t g, std::uint8_t* dst,
-                        const std::vector<std::pair<const std::uint8_t*, std::uint64_t>>& pieces) {
-    Gpu& gpu = *gpus_[g];
-    DeviceGuard guard;
-    gpu.bind();
-    std::uint64_t total = 0;
-    for (const auto& pc : pieces) total += pc.second;
-    if (total == 0) return;
-    if (pieces.size() == 1 && total < kDirectBytes) {
-      check(ucg_memcpy_h2d(dst, pieces[0].first, total, gpu.stream()));
-      return;
-    }
-    Staging& s = ensure_staging(g);
-    ensure_copy_pool();
-    std::uint8_t* stage = nullptr;
-    std::uint64_t fill = 0, dev_off = 0;
-    int k = 0;
-    auto acquire = [&] {
-      k = s.next;
-      s.next ^= 1;
-      if (s.busy[k]) check(ucg_event_synchronize(s.ev[k]));  // that half's previous DMA is done
-      stage = static_cast<std::uint8_t*>(s.buf[k]);
-      fill = 0;
-    };
-    auto flush = [&] {
-      if (!fill) return;
-      check(ucg_memcpy_h2d(dst + dev_off, stage, fill, gpu.stream()));
-      check(ucg_event_record(s.ev[k], gpu.stream()));
-      s.busy[k] = true;
-      dev_off += fill;
-      fill = 0;
-      stage = nullptr;
-    };
-    for (const auto& [src, n] : pieces) {
-      for (std::uint64_t off = 0; off < n;) {
-        if (!stage) acquire();
-        const std::uint64_t len = std::min(kStageBytes - fill, n - off);
-        copy_pool_->copy(stage + fill, src + off, len);  // all host threads for large pieces
-        fill += len;
-        off += len;
-        if (fill == kStageBytes) flush();
+  // -- host threads ------------------------------------------------------------------
+  // fn(g) for every GPU, each on its own host thread (GPU 0 on the caller's)
+  void run_per_gpu(const std::function<void(std::size_t)>& fn) {
+    std::vector<std::thread> t;
+    std::vector<std::exception_ptr> err(gpus_.size());
+    auto one = [&](std::size_t g) {
+      try {
+        DeviceGuard guard;
+        gpus_[g]->bind();
+        fn(g);
+      } catch (...) {
+        err[g] = std::current_exception();
       }
-    }
-    flush();
-  }
-
-  Staging& ensure_staging(std::size_t g) {
-    if (staging_.size() < gpus_.size()) staging_.resize(gpus_.size());
-    Staging& s = staging_[g];
-    if (!s.buf[0]) {
-      DeviceGuard guard;
-      gpus_[g]->bind();
-      for (int k = 0; k < 2; ++k) {
-        check(ucg_host_alloc(&s.buf[k], kStageBytes));
-        check(ucg_event_create(&s.ev[k]));
-      }
-    }
-    return s;
-  }
-  void ensure_copy_pool() {
-    if (copy_pool_) return;
-    unsigned n = std::max(1u, std::thread::hardware_concurrency());
-    if (const char* e = std::getenv("UCG_COPY_THREADS")) n = std::max(1, std::atoi(e));  // A/B runs
-    copy_pool_ = std::make_unique<CopyPool>(n);
+    };
+    for (std::size_t g = 1; g < gpus_.size(); ++g) t.emplace_back(one, g);
+    one(0);
+    for (auto& x : t) x.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
   }
 
   // -- helpers ----------------------------------------------------------------------
@@ -777,20 +666,33 @@ class DeviceEngine {
   /// over the same dataset shape reuses them. Ops run one at a time per
   /// engine and finish before returning, so a table is never in flight twice.
   ucg_segtab* segtab(std::size_t g, const std::vector<std::uint64_t>& begin, const std::vector<std::uint64_t>& len) {
-    std::string key = std::to_string(g) + ":";
-    key.append(reinterpret_cast<const char*>(begin.data()), begin.size() * 8);
-    key.append(reinterpret_cast<const char*>(len.data()), len.size() * 8);
-    for (auto& [k, t] : tabs_)
-      if (k == key) return t.get();
+    // keyed by (GPU, FNV-1a of the layout); the layout itself confirms a hit.
+    // At most kMaxTabs live tables, least recently used evicted first.
+    std::uint64_t h = 0xcbf29ce484222325ull ^ g;
+    for (const auto* v : {&begin, &len})
+      for (std::uint64_t x : *v) h = (h ^ x) * 0x100000001b3ull;
+    for (auto it = tabs_.begin(); it != tabs_.end(); ++it) {
+      if (it->gpu == g && it->hash == h && it->begin == begin && it->len == len) {
+        tabs_.splice(tabs_.begin(), tabs_, it);  // most recent first
+        return tabs_.front().tab.get();
+      }
+    }
     ucg_segtab* tab = nullptr;
     check(ucg_segtab_create(begin.data(), len.data(), begin.size(), &tab));
-    if (tabs_.size() >= 16) tabs_.erase(tabs_.begin());
-    tabs_.emplace_back(std::move(key), std::unique_ptr<ucg_segtab, TabFree>(tab));
+    if (tabs_.size() >= kMaxTabs) tabs_.pop_back();
+    tabs_.push_front(Tab{g, h, begin, len, std::unique_ptr<ucg_segtab, TabFree>(tab)});
     return tab;
   }
   struct TabFree {
     void operator()(ucg_segtab* t) const { ucg_segtab_destroy(t); }
   };
+  struct Tab {
+    std::size_t gpu;
+    std::uint64_t hash;
+    std::vector<std::uint64_t> begin, len;
+    std::unique_ptr<ucg_segtab, TabFree> tab;
+  };
+  static constexpr std::size_t kMaxTabs = 16;
 
   void sync_all() {
     for (auto& g : gpus_) {
@@ -803,9 +705,7 @@ class DeviceEngine {
   WorkloadParams params_;
   std::vector<std::shared_ptr<Gpu>> gpus_;
   std::shared_ptr<DevicePool> pool_ = std::make_shared<DevicePool>();
-  std::vector<std::pair<std::string, std::unique_ptr<ucg_segtab, TabFree>>> tabs_;
-  std::vector<Staging> staging_;
-  std::unique_ptr<CopyPool> copy_pool_;
+  std::list<Tab> tabs_;
 };
 
 }  // namespace ucores_b200

@@ -29,6 +29,7 @@
 #include "ucores/kernel.hpp"
 #include "ucores/task.hpp"
 #include "ucores_b200/gpu_context.hpp"
+#include "ucores_b200/host_pipe.hpp"
 #include "ucores_b200/kernels.hpp"
 
 namespace ucores_b200 {
@@ -100,54 +101,39 @@ inline std::vector<std::uint64_t> pack_offsets(const std::vector<std::uint64_t>&
   return off;
 }
 
-inline int op_code(kernels::ReduceOp op) { return op == kernels::ReduceOp::Max ? UCG_OP_MAX : UCG_OP_SUM; }
-
-// Many small payloads (a wave of one-float elements) move as ONE DMA through
-// the GPU's pinned staging; large ones go directly, one copy each.
-inline bool pack_pieces(std::size_t count, std::uint64_t bytes) {
-  return count > 8 && bytes / count < (256u << 10);
+template <class T>
+std::vector<std::span<const std::uint8_t>> as_bytes(const std::vector<std::span<const T>>& in) {
+  std::vector<std::span<const std::uint8_t>> b;
+  b.reserve(in.size());
+  for (const auto& v : in) b.emplace_back(reinterpret_cast<const std::uint8_t*>(v.data()), v.size_bytes());
+  return b;
+}
+inline std::vector<std::uint64_t> scaled(const std::vector<std::uint64_t>& v, std::uint64_t k) {
+  std::vector<std::uint64_t> o(v.size());
+  for (std::size_t i = 0; i < v.size(); ++i) o[i] = v[i] * k;
+  return o;
 }
 
-// Host -> device: piece i lands at element offset off[i] of dst.
+/// Elements out of a pipe download (the vectors are complete after drain()).
 template <class T>
-void upload_pieces(Gpu& g, T* dst, const std::vector<std::span<const T>>& in, const std::vector<std::uint64_t>& off,
-                   int stage_slot = 0) {
-  if (in.empty()) return;
-  std::uint64_t bytes = 0;
-  for (const auto& v : in) bytes += v.size_bytes();
-  if (pack_pieces(in.size(), bytes)) {
-    const std::uint64_t extent = off.back() + in.back().size();
-    T* h = static_cast<T*>(g.host_stage(stage_slot, std::max<std::uint64_t>(extent, 1) * sizeof(T)));
-    for (std::size_t i = 0; i < in.size(); ++i)
-      if (!in[i].empty()) std::memcpy(h + off[i], in[i].data(), in[i].size_bytes());
-    g.h2d(dst, h, extent * sizeof(T));
-  } else {
-    for (std::size_t i = 0; i < in.size(); ++i) g.h2d(dst + off[i], in[i].data(), in[i].size_bytes());
-  }
-}
-
-// Device -> host: piece i (sizes[i] elements at offset off[i] of src) into its
-// own vector. Synchronises the GPU's stream.
-template <class T>
-std::vector<std::vector<T>> download_pieces(Gpu& g, const T* src, const std::vector<std::uint64_t>& sizes,
-                                            const std::vector<std::uint64_t>& off, int stage_slot = 1) {
-  std::vector<std::vector<T>> out(sizes.size());
-  std::uint64_t bytes = 0;
-  for (std::uint64_t n : sizes) bytes += n * sizeof(T);
-  if (!sizes.empty() && pack_pieces(sizes.size(), bytes)) {
-    const std::uint64_t extent = off.back() + sizes.back();
-    T* h = static_cast<T*>(g.host_stage(stage_slot, std::max<std::uint64_t>(extent, 1) * sizeof(T)));
-    g.d2h(h, src, extent * sizeof(T));
-    g.sync();
-    for (std::size_t i = 0; i < sizes.size(); ++i) out[i].assign(h + off[i], h + off[i] + sizes[i]);
-  } else {
-    for (std::size_t i = 0; i < sizes.size(); ++i) {
-      out[i].resize(sizes[i]);
-      g.d2h(out[i].data(), src + off[i], sizes[i] * sizeof(T));
-    }
-    g.sync();
+std::vector<ucores::Element> to_elements(std::vector<std::vector<T>>&& v) {
+  std::vector<ucores::Element> out;
+  out.reserve(v.size());
+  for (auto& x : v) {
+    if constexpr (std::is_same_v<T, float>) out.push_back(ucores::Element::f32(std::move(x)));
+    else if constexpr (std::is_same_v<T, std::int64_t>) out.push_back(ucores::Element::i64(std::move(x)));
+    else out.push_back(ucores::Element::bytes(std::move(x)));
   }
   return out;
+}
+
+inline int op_code(kernels::ReduceOp op) { return op == kernels::ReduceOp::Max ? UCG_OP_MAX : UCG_OP_SUM; }
+
+// Many small payloads (a wave of one-float elements) move packed through the
+// pipe's pinned slots and run as ONE launch; large ones stream element by
+// element (host_pipe.hpp).
+inline bool pack_pieces(std::size_t count, std::uint64_t bytes) {
+  return count > 8 && bytes / count < (256u << 10);
 }
 
 }  // namespace detail
@@ -165,16 +151,35 @@ inline DeviceOp affine_f32(float a, float b) {
       in.push_back(detail::input_view<float>(tasks[i]->inputs.at(0), i));
       sizes.push_back(in.back().size());
     }
+    std::uint64_t bytes = 0;
+    for (std::uint64_t n : sizes) bytes += n * 4;
+    const bool packed = detail::pack_pieces(in.size(), bytes);
+    // packed: back to back (the flat map does not care where elements
+    // start); streamed: each element on a 256-byte boundary
     std::uint64_t total = 0;
-    const auto off = detail::pack_offsets(sizes, 64, &total);
+    const auto off = detail::pack_offsets(sizes, packed ? 1 : 64, &total);
     float* x = static_cast<float*>(g.scratch(0).ensure(total * 4));
     float* y = static_cast<float*>(g.scratch(1).ensure(total * 4));
-    detail::upload_pieces(g, x, in, off);
-    check(ucg_map_affine_f32(x, y, total, a, b, g.stream()));
-    std::vector<ucores::Element> out;
-    out.reserve(in.size());
-    for (auto& v : detail::download_pieces<float>(g, y, sizes, off)) out.push_back(ucores::Element::f32(std::move(v)));
-    return out;
+    HostPipe& pipe = g.attached<HostPipe>();
+    std::vector<std::vector<float>> outs(in.size());
+    if (packed) {
+      // many small elements: packed into slots, one launch, packed back
+      pipe.upload_pieces(x, detail::as_bytes(in), detail::scaled(off, 4));
+      pipe.compute_after_upload();
+      check(ucg_map_affine_f32(x, y, total, a, b, g.stream()));
+      pipe.download_pieces(&outs, y, sizes, off);
+    } else {
+      // per element: its upload, its launch as soon as it lands, its
+      // download while the next element is copied in
+      for (std::size_t i = 0; i < in.size(); ++i) {
+        pipe.upload(x + off[i], in[i].data(), in[i].size_bytes());
+        pipe.compute_after_upload();
+        check(ucg_map_affine_f32(x + off[i], y + off[i], sizes[i], a, b, g.stream()));
+        pipe.download(&outs[i], y + off[i], sizes[i]);
+      }
+    }
+    pipe.drain();
+    return detail::to_elements(std::move(outs));
   };
   op.run_phase = [a, b](Gpu& g, ucores::KernelContext& ctx) {
     auto x = ctx.buffer<float>("x");
@@ -204,7 +209,9 @@ inline DeviceOp partition_reduce_f32(kernels::ReduceOp rop) {
     std::uint64_t total = 0;
     const auto off = detail::pack_offsets(sizes, 64, &total);
     float* x = static_cast<float*>(g.scratch(0).ensure(total * 4));
-    detail::upload_pieces(g, x, in, off);
+    HostPipe& pipe = g.attached<HostPipe>();
+    pipe.upload_pieces(x, detail::as_bytes(in), detail::scaled(off, 4));
+    pipe.compute_after_upload();
     ucg_segtab* tab = nullptr;
     check(ucg_segtab_create(off.data(), sizes.data(), sizes.size(), &tab));
     std::uint64_t nscratch = 0;
@@ -214,7 +221,12 @@ inline DeviceOp partition_reduce_f32(kernels::ReduceOp rop) {
     const int rc = ucg_segment_reduce_f32(x, tab, code, scratch, part, g.stream());
     std::vector<float> host(sizes.size());
     if (rc == UCG_OK) g.d2h(host.data(), part, host.size() * 4);
-    g.sync();
+    try {
+      pipe.drain();
+    } catch (...) {
+      ucg_segtab_destroy(tab);
+      throw;
+    }
     ucg_segtab_destroy(tab);
     check(rc);
     std::vector<ucores::Element> out;
@@ -266,16 +278,16 @@ std::vector<ucores::Element> elementwise_tasks(Gpu& g, TaskBatch tasks, int code
   T* a = static_cast<T*>(g.scratch(0).ensure(total * sizeof(T)));
   T* b = static_cast<T*>(g.scratch(1).ensure(total * sizeof(T)));
   T* c = static_cast<T*>(g.scratch(2).ensure(total * sizeof(T)));
-  detail::upload_pieces(g, a, A, off, 0);
-  detail::upload_pieces(g, b, B, off, 2);
+  HostPipe& pipe = g.attached<HostPipe>();
+  pipe.upload_pieces(a, detail::as_bytes(A), detail::scaled(off, sizeof(T)));
+  pipe.upload_pieces(b, detail::as_bytes(B), detail::scaled(off, sizeof(T)));
+  pipe.compute_after_upload();
   if constexpr (std::is_same_v<T, float>) check(ucg_elementwise2_f32(a, b, c, total, code, g.stream()));
   else check(ucg_elementwise2_i64(a, b, c, total, g.stream()));
-  std::vector<ucores::Element> out;
-  for (auto& v : detail::download_pieces<T>(g, c, sizes, off)) {
-    if constexpr (std::is_same_v<T, float>) out.push_back(ucores::Element::f32(std::move(v)));
-    else out.push_back(ucores::Element::i64(std::move(v)));
-  }
-  return out;
+  std::vector<std::vector<T>> outs;
+  pipe.download_pieces(&outs, c, sizes, off);
+  pipe.drain();
+  return detail::to_elements(std::move(outs));
 }
 
 template <class T>
@@ -370,13 +382,15 @@ inline DeviceOp sobel(std::size_t width) {
     const auto out_off = detail::pack_offsets(out_sz, 16, &tout);
     std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(tin));
     std::uint8_t* dout = static_cast<std::uint8_t*>(g.scratch(1).ensure(tout));
-    detail::upload_pieces(g, din, in, in_off);
+    HostPipe& pipe = g.attached<HostPipe>();
+    pipe.upload_pieces(din, in, in_off);
+    pipe.compute_after_upload();
     check(ucg_sobel_bands_u8(din, in_off.data(), dout, out_off.data(), rows.data(), rows.size(), width,
                              g.stream()));
-    std::vector<ucores::Element> out;
-    for (auto& v : detail::download_pieces<std::uint8_t>(g, dout, out_sz, out_off))
-      out.push_back(ucores::Element::bytes(std::move(v)));
-    return out;
+    std::vector<std::vector<std::uint8_t>> outs;
+    pipe.download_pieces(&outs, dout, out_sz, out_off);
+    pipe.drain();
+    return detail::to_elements(std::move(outs));
   };
   op.run_phase = [width](Gpu& g, ucores::KernelContext& ctx) {
     auto in = ctx.buffer<std::uint8_t>("in");
@@ -410,14 +424,16 @@ inline DeviceOp wordcount(std::uint64_t min_device_bytes) {
     const auto off = detail::pack_offsets(sizes, 16, &total);
     std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(total));
     std::uint8_t* dfl = static_cast<std::uint8_t*>(g.scratch(1).ensure(total));
+    HostPipe& pipe = g.attached<HostPipe>();
+    pipe.upload_pieces(din, in, off);
+    pipe.compute_after_upload();
     for (std::size_t i = 0; i < in.size(); ++i) {
       if (sizes[i] < min_device_bytes || !sizes[i]) continue;
-      g.h2d(din + off[i], in[i].data(), sizes[i]);
       check(ucg_word_start_flags(din + off[i], sizes[i], dfl + off[i], g.stream()));
     }
-    std::vector<std::uint8_t> flags(total);
-    g.d2h(flags.data(), dfl, total);
-    g.sync();
+    std::vector<std::uint8_t> flags;
+    pipe.download(&flags, dfl, total);
+    pipe.drain();
     std::vector<ucores::Element> out;
     for (std::size_t i = 0; i < in.size(); ++i) {
       if (sizes[i] < min_device_bytes) out.push_back(kernels::WordCount::table_host(in[i]));
@@ -453,16 +469,25 @@ inline DeviceOp matmul_tc(std::size_t n, bool fp32_faithful = true) {
     g.d2h(c_host, dc, n * n * 4);
     g.sync();
   };
-  op.run_tasks = [n, body](Gpu& g, TaskBatch tasks) {
-    std::vector<ucores::Element> out;
+  op.run_tasks = [n, fp32_faithful](Gpu& g, TaskBatch tasks) {
+    std::vector<std::vector<float>> outs(tasks.size());
     for (std::size_t i = 0; i < tasks.size(); ++i) {
       auto ab = detail::input_view<float>(tasks[i]->inputs.at(0), i);
       if (ab.size() != 2 * n * n) throw TaskFailure(i, "map_parameters", "matmul element must hold A||B");
-      std::vector<float> c(n * n);
-      body(g, ab.data(), c.data());
-      out.push_back(ucores::Element::f32(std::move(c)));
     }
-    return out;
+    // two device slots: task i+1's upload overlaps task i's product, task
+    // i's C download overlaps task i+1's
+    HostPipe& pipe = g.attached<HostPipe>();
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+      float* dab = static_cast<float*>(g.scratch(4 + 2 * (i & 1)).ensure(2 * n * n * 4));
+      float* dc = static_cast<float*>(g.scratch(5 + 2 * (i & 1)).ensure(n * n * 4));
+      pipe.upload(dab, tasks[i]->inputs[0].as_f32().data(), 2 * n * n * 4);
+      pipe.compute_after_upload();
+      check((fp32_faithful ? ucg_gemm_f32 : ucg_gemm_tf32)(dab, dab + n * n, dc, n, g.stream()));
+      pipe.download(&outs[i], dc, n * n);
+    }
+    pipe.drain();
+    return detail::to_elements(std::move(outs));
   };
   op.run_phase = [body](Gpu& g, ucores::KernelContext& ctx) {
     auto ab = ctx.buffer<float>("ab");

@@ -94,6 +94,7 @@ class Gpu {
   Gpu(const Gpu&) = delete;
   Gpu& operator=(const Gpu&) = delete;
   ~Gpu() {
+    attach_.reset();  // the attachment (HostPipe) drains this GPU's streams first
     for (Stage& st : stages_)
       if (st.ptr) ucg_host_free(st.ptr);
     if (stream_) {
@@ -132,6 +133,15 @@ class Gpu {
   /// Serialises use of this GPU's stream/scratch between host threads.
   std::mutex& mutex() { return mu_; }
 
+  /// One T per GPU (T(Gpu&)), created on first use and destroyed before the
+  /// GPU's stream: the transfer pipeline (host_pipe.hpp) lives here.
+  template <class T>
+  T& attached() {
+    std::lock_guard<std::mutex> lk(attach_mu_);
+    if (!attach_) attach_ = std::make_shared<T>(*this);
+    return *static_cast<T*>(attach_.get());
+  }
+
   void h2d(void* dst, const void* src, std::uint64_t bytes) { check(ucg_memcpy_h2d(dst, src, bytes, stream_)); }
   void d2h(void* dst, const void* src, std::uint64_t bytes) { check(ucg_memcpy_d2h(dst, src, bytes, stream_)); }
 
@@ -145,6 +155,8 @@ class Gpu {
   std::vector<DeviceBuffer> scratch_;
   std::vector<Stage> stages_;
   std::mutex mu_;
+  std::mutex attach_mu_;
+  std::shared_ptr<void> attach_;
 };
 
 /// Number of CUDA devices visible (0 when none; never throws for "no device").
