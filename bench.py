@@ -444,8 +444,14 @@ def our_arm(args, world, rank, local):
             from paper_1505_01120_b200 import engine_capi
 
             xs = np.concatenate([pipe.x[b:b + n].cpu().numpy() for b, n in zip(pipe.layout.begins, pipe.local_lens)])
-            _, _, r_eng, sec = engine_capi.pipeline_f32(xs, pipe.local_lens, op=args.op, want_y=False)
+            bd = engine_capi.pipeline_breakdown_f32(xs, pipe.local_lens, op=args.op)
+            sec = bd["total_s"]
+            r_eng = np.array([int(bd["result_bits"], 16)], np.uint32).view(np.float32)[0]
             engine_e2e = {"value": n_total / sec, "unit": UNIT, "seconds": sec,
+                          "breakdown_s": {k: round(v, 4) for k, v in bd.items() if k.endswith("_s")},
+                          "bound": ("the reference Engine's own work (engine_own_s: it copies every task input "
+                                    "twice and concatenates every partition, single-threaded into fresh memory) "
+                                    "— the driver's waves are *_wave_s"),
                           "path": "ucores::Engine map_cl/map_cl_partition/reduce_cl + GpuClusterDriver (seam A), "
                                   "from a built host Dataset to the result Element (as the reference arm)",
                           "result_matches": bool(np.float32(r_eng) == np.float32(result))}

@@ -170,12 +170,15 @@ inline DeviceOp affine_f32(float a, float b) {
       pipe.download_pieces(&outs, y, sizes, off);
     } else {
       // per element: its upload, its launch as soon as it lands, its
-      // download while the next element is copied in
+      // download while the next element is copied in; the output vectors
+      // are allocated by pool threads meanwhile
+      std::vector<std::shared_ptr<WorkPool::Done>> ready(in.size());
+      for (std::size_t i = 0; i < in.size(); ++i) ready[i] = pipe.prepare(&outs[i], sizes[i]);
       for (std::size_t i = 0; i < in.size(); ++i) {
         pipe.upload(x + off[i], in[i].data(), in[i].size_bytes());
         pipe.compute_after_upload();
         check(ucg_map_affine_f32(x + off[i], y + off[i], sizes[i], a, b, g.stream()));
-        pipe.download(&outs[i], y + off[i], sizes[i]);
+        pipe.download(&outs[i], y + off[i], sizes[i], ready[i]);
       }
     }
     pipe.drain();

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <atomic>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <optional>
 #include <string>
@@ -49,33 +50,35 @@ class GpuClusterDriver : public ucores::ClusterDriver {
   GpuClusterDriver(const ucores::KernelRegistry& registry, const DeviceOpRegistry& ops, Options opt)
       : registry_(&registry), ops_(&ops), opt_(opt) {
     for (auto& g : open_gpus(opt.max_gpus)) gpus_.push_back(std::shared_ptr<Gpu>(std::move(g)));
-    for (auto& g : gpus_)
-      workers_.push_back(std::make_unique<GpuWorkerRuntime>("gpu" + std::to_string(g->ordinal()), registry, ops, g));
+    for (auto& g : gpus_) {
+      worker_ids_.push_back("gpu" + std::to_string(g->ordinal()));
+      workers_.push_back(std::make_unique<GpuWorkerRuntime>(worker_ids_.back(), registry, ops, g));
+    }
   }
 
   std::uint64_t new_job_id() override { return ++job_id_; }
 
   std::vector<ucores::TaskResult> run_wave(std::vector<ucores::Task> tasks, int max_retries) override {
     if (tasks.empty()) return {};
-    std::vector<std::optional<ucores::TaskResult>> done(tasks.size());
+    // results are filled in place (a wave of the C1 literal form is 2^20
+    // tasks: no per-task optional / failure slots)
+    Wave w;
+    w.out.resize(tasks.size());
     if (opt_.mode == Mode::PerTask) {
-      run_per_task(tasks, max_retries, done);
+      run_per_task(tasks, max_retries, w);
     } else {
       // group by kernel name, keeping task order inside each group
       std::map<std::string, std::vector<std::size_t>> groups;
       for (std::size_t i = 0; i < tasks.size(); ++i) groups[tasks[i].kernel_name].push_back(i);
-      for (auto& [name, idx] : groups) run_group(tasks, name, idx, max_retries, done);
+      for (auto& [name, idx] : groups) run_group(tasks, name, idx, max_retries, w);
     }
-    std::vector<ucores::TaskResult> out;
-    out.reserve(tasks.size());
-    for (auto& r : done) out.push_back(std::move(*r));
     // results sorted by task_id (scheduler.hpp:274-287); a wave the Engine
     // planned in task order already is (sorting 2^20 results costs ~0.1 s)
     auto by_id = [](const ucores::TaskResult& a, const ucores::TaskResult& b) { return a.task_id < b.task_id; };
-    if (!std::is_sorted(out.begin(), out.end(), by_id)) std::sort(out.begin(), out.end(), by_id);
+    if (!std::is_sorted(w.out.begin(), w.out.end(), by_id)) std::sort(w.out.begin(), w.out.end(), by_id);
     waves_ += 1;
     tasks_ += tasks.size();
-    return out;
+    return std::move(w.out);
   }
 
   // -- observability (mirrors LocalClusterDriver's hooks) ---------------------
@@ -90,15 +93,25 @@ class GpuClusterDriver : public ucores::ClusterDriver {
   struct Failure {
     std::string phase, detail;
   };
+  // One wave's results (in task order) and its failed tasks (sparse;
+  // guarded, batches of different GPUs report concurrently).
+  struct Wave {
+    std::vector<ucores::TaskResult> out;
+    std::map<std::size_t, Failure> failed;
+    std::mutex mu;
+    void fail(std::size_t i, Failure f) {
+      std::lock_guard<std::mutex> lk(mu);
+      failed[i] = std::move(f);
+    }
+  };
 
   // Run tasks idx[lo,hi) of one kernel on GPU g as one batch. On failure the
   // batch is re-run task by task so only the failing tasks are retried.
   void run_batch(const std::vector<ucores::Task>& tasks, const DeviceOp& op, const std::vector<std::size_t>& idx,
-                 std::size_t lo, std::size_t hi, std::size_t g,
-                 std::vector<std::optional<ucores::TaskResult>>& done,
-                 std::vector<std::optional<Failure>>& failed) {
+                 std::size_t lo, std::size_t hi, std::size_t g, Wave& w) {
     if (lo >= hi) return;
     std::vector<const ucores::Task*> batch;
+    batch.reserve(hi - lo);
     for (std::size_t k = lo; k < hi; ++k) batch.push_back(&tasks[idx[k]]);
     Gpu& gpu = *gpus_[g];
     auto attempt = [&](std::span<const ucores::Task* const> b) {
@@ -109,18 +122,18 @@ class GpuClusterDriver : public ucores::ClusterDriver {
     };
     try {
       std::vector<ucores::Element> outs = attempt(batch);
-      for (std::size_t k = 0; k < batch.size(); ++k) done[idx[lo + k]] = make_result(*batch[k], std::move(outs[k]), g);
+      for (std::size_t k = 0; k < batch.size(); ++k) fill_result(w.out[idx[lo + k]], *batch[k], std::move(outs[k]), g);
     } catch (const std::exception&) {
       for (std::size_t k = 0; k < batch.size(); ++k) {
         try {
           std::vector<ucores::Element> one = attempt(std::span<const ucores::Task* const>(&batch[k], 1));
-          done[idx[lo + k]] = make_result(*batch[k], std::move(one.at(0)), g);
+          fill_result(w.out[idx[lo + k]], *batch[k], std::move(one.at(0)), g);
         } catch (const TaskFailure& f) {
-          failed[idx[lo + k]] = Failure{f.phase(), f.what()};
+          w.fail(idx[lo + k], Failure{f.phase(), f.what()});
         } catch (const ucores::KernelPanic& e) {
-          failed[idx[lo + k]] = Failure{e.phase(), e.what()};
+          w.fail(idx[lo + k], Failure{e.phase(), e.what()});
         } catch (const std::exception& e) {
-          failed[idx[lo + k]] = Failure{"run", e.what()};
+          w.fail(idx[lo + k], Failure{"run", e.what()});
         }
       }
     }
@@ -128,12 +141,11 @@ class GpuClusterDriver : public ucores::ClusterDriver {
   }
 
   void run_group(const std::vector<ucores::Task>& tasks, const std::string& name, const std::vector<std::size_t>& idx,
-                 int max_retries, std::vector<std::optional<ucores::TaskResult>>& done) {
+                 int max_retries, Wave& w) {
     per_gpu_.resize(gpus_.size(), 0);
     const DeviceOp* op = ops_->find(name);
-    std::vector<std::optional<Failure>> failed(tasks.size());
     if (!op || !op->run_tasks) {
-      for (std::size_t i : idx) failed[i] = Failure{"run", "no device body for kernel '" + name + "' (no CPU fallback)"};
+      for (std::size_t i : idx) w.fail(i, Failure{"run", "no device body for kernel '" + name + "' (no CPU fallback)"});
     } else {
       const std::size_t T = idx.size(), G = std::min(gpus_.size(), T);
       std::vector<std::thread> threads;
@@ -141,29 +153,35 @@ class GpuClusterDriver : public ucores::ClusterDriver {
       for (std::size_t g = 1; g < G; ++g) {
         threads.emplace_back([&, g] {
           try {
-            run_batch(tasks, *op, idx, g * T / G, (g + 1) * T / G, g, done, failed);
+            run_batch(tasks, *op, idx, g * T / G, (g + 1) * T / G, g, w);
           } catch (...) {
             errs[g] = std::current_exception();
           }
         });
       }
-      run_batch(tasks, *op, idx, 0, T / G, 0, done, failed);
+      run_batch(tasks, *op, idx, 0, T / G, 0, w);
       for (auto& t : threads) t.join();
       for (auto& e : errs)
         if (e) std::rethrow_exception(e);
     }
     // retries: attempt 1..max_retries on the next GPU (scheduler.hpp:290-302)
-    for (std::size_t i : idx) {
-      if (!failed[i]) continue;
-      std::optional<Failure> last = failed[i];
+    std::map<std::size_t, Failure> failed;
+    failed.swap(w.failed);
+    for (auto& [i, first] : failed) {
+      std::optional<Failure> last = first;
       for (int a = 1; a <= max_retries && last; ++a) {
         ++retries_;
         const std::size_t g = (i + a) % gpus_.size();
-        std::vector<std::optional<Failure>> f1(tasks.size());
+        last.reset();
         if (op && op->run_tasks) {
           std::vector<std::size_t> one{i};
-          run_batch(tasks, *op, one, 0, 1, g, done, f1);
-          last = f1[i];
+          run_batch(tasks, *op, one, 0, 1, g, w);
+          if (auto it = w.failed.find(i); it != w.failed.end()) {
+            last = it->second;
+            w.failed.erase(it);
+          }
+        } else {
+          last = first;
         }
       }
       if (last) {
@@ -174,8 +192,7 @@ class GpuClusterDriver : public ucores::ClusterDriver {
     }
   }
 
-  void run_per_task(const std::vector<ucores::Task>& tasks, int max_retries,
-                    std::vector<std::optional<ucores::TaskResult>>& done) {
+  void run_per_task(const std::vector<ucores::Task>& tasks, int max_retries, Wave& w) {
     per_gpu_.resize(gpus_.size(), 0);
     const std::size_t T = tasks.size(), G = std::min(gpus_.size(), T);
     std::vector<std::optional<std::string>> failure(T);
@@ -185,7 +202,7 @@ class GpuClusterDriver : public ucores::ClusterDriver {
           const std::size_t gg = (g + a) % gpus_.size();
           ucores::Message m = workers_[gg]->execute(tasks[i]);
           if (auto* r = std::get_if<ucores::TaskResultMsg>(&m)) {
-            done[i] = std::move(r->result);
+            w.out[i] = std::move(r->result);
             break;
           }
           const auto& e = std::get<ucores::TaskErrorMsg>(m);
@@ -206,11 +223,10 @@ class GpuClusterDriver : public ucores::ClusterDriver {
       if (f) throw ucores::JobFailed(*f);
   }
 
-  ucores::TaskResult make_result(const ucores::Task& t, ucores::Element out, std::size_t g) const {
-    ucores::TaskResult r;
+  void fill_result(ucores::TaskResult& r, const ucores::Task& t, ucores::Element out, std::size_t g) const {
     r.job_id = t.job_id;
     r.task_id = t.task_id;
-    r.worker_id = "gpu" + std::to_string(gpus_[g]->ordinal());
+    r.worker_id = worker_ids_[g];
     std::uint64_t in_bytes = 0, items = 0;
     for (const auto& e : t.inputs) {
       in_bytes += e.byte_size();
@@ -221,7 +237,6 @@ class GpuClusterDriver : public ucores::ClusterDriver {
     r.metrics.executor_kind = "cuda-sm100a";
     r.metrics.device_invocations = 1;
     r.output = std::move(out);
-    return r;
   }
 
   const ucores::KernelRegistry* registry_;
@@ -229,6 +244,7 @@ class GpuClusterDriver : public ucores::ClusterDriver {
   Options opt_;
   std::vector<std::shared_ptr<Gpu>> gpus_;
   std::vector<std::unique_ptr<GpuWorkerRuntime>> workers_;
+  std::vector<std::string> worker_ids_;
   std::atomic<std::uint64_t> job_id_{0};
   std::uint64_t waves_ = 0, tasks_ = 0, retries_ = 0;
   std::vector<std::uint64_t> per_gpu_;

@@ -185,7 +185,8 @@ inline WorkPool& work_pool() {
 class HostPipe {
  public:
   static constexpr std::uint64_t kSlotBytes = 32ull << 20;
-  static constexpr int kSlots = 6;
+  static constexpr int kSlots = 8;
+  static constexpr int kDrainSplit = 4;
 
   explicit HostPipe(Gpu& g) : gpu_(&g) {
     DeviceGuard guard;
@@ -284,37 +285,42 @@ class HostPipe {
     check(ucg_stream_wait_event(gpu_->stream(), h2d_ev_));
   }
 
-  /// Device -> a new host vector of `n` entries, through the out ring; the
-  /// D2H waits for the compute stream's work so far. Returns immediately:
-  /// the vector is complete after drain().
+  /// Allocates `dst` (n entries) on a pool thread, so the page faults of the
+  /// output vectors are taken in parallel and ahead of their data. Returns
+  /// the allocation's latch for download().
   template <class T>
-  void download(std::vector<T>* dst, const T* dev, std::uint64_t n) {
+  std::shared_ptr<WorkPool::Done> prepare(std::vector<T>* dst, std::uint64_t n) {
+    return work_pool().submit([dst, n] { dst->resize(n); });
+  }
+
+  /// Device -> host vector `dst` of `n` entries (allocated by prepare(), or
+  /// here), through the out ring; the D2H waits for the compute stream's work
+  /// so far. Returns immediately: `dst` is complete after drain(). Each slot
+  /// is drained by kDrainSplit pool tasks copying disjoint slices.
+  template <class T>
+  void download(std::vector<T>* dst, const T* dev, std::uint64_t n,
+                std::shared_ptr<WorkPool::Done> ready = nullptr) {
+    if (!ready) ready = prepare(dst, n);
     check(ucg_event_record(compute_ev_, gpu_->stream()));
     check(ucg_stream_wait_event(d2h_, compute_ev_));
     const std::uint64_t bytes = n * sizeof(T);
-    if (bytes == 0) {
-      dst->clear();
-      return;
-    }
-    // one drain task per chunk; a vector's tasks run in chunk order (each
-    // waits for its predecessor, which the FIFO pool started first)
-    const std::uint64_t chunk = kSlotBytes / sizeof(T) * sizeof(T);
-    std::shared_ptr<WorkPool::Done> prev;
-    for (std::uint64_t off = 0; off < bytes; off += chunk) {
-      const std::uint64_t m = std::min(chunk, bytes - off);
+    for (std::uint64_t off = 0; off < bytes; off += kSlotBytes) {
+      const std::uint64_t m = std::min(kSlotBytes, bytes - off);
       Slot& s = acquire_out();
       check(ucg_memcpy_d2h(s.buf, reinterpret_cast<const std::uint8_t*>(dev) + off, m, d2h_));
       check(ucg_event_record(s.ev, d2h_));
-      s.draining.store(true);
-      prev = work_pool().submit([dst, n, m, &s, prev] {
-        if (prev) prev->wait();
-        check(ucg_event_synchronize(s.ev));
-        if (dst->capacity() < n) dst->reserve(n);
-        const T* h = static_cast<const T*>(s.buf);
-        dst->insert(dst->end(), h, h + m / sizeof(T));
-        s.draining.store(false);
-      });
-      pending_.push_back(prev);
+      const int parts = m >= (4u << 20) ? kDrainSplit : 1;
+      s.drains.store(parts);
+      for (int k = 0; k < parts; ++k) {
+        const std::uint64_t b = m * k / parts, e = m * (k + 1) / parts;
+        pending_.push_back(work_pool().submit([dst, off, b, e, &s, ready] {
+          ready->wait();
+          check(ucg_event_synchronize(s.ev));
+          std::memcpy(reinterpret_cast<std::uint8_t*>(dst->data()) + off + b,
+                      static_cast<const std::uint8_t*>(s.buf) + b, e - b);
+          s.drains.fetch_sub(1);
+        }));
+      }
     }
   }
 
@@ -341,13 +347,19 @@ class HostPipe {
       const std::uint64_t extent = (off[j - 1] + sizes[j - 1] - base) * sizeof(T);
       check(ucg_memcpy_d2h(s.buf, dev + base, extent, d2h_));
       check(ucg_event_record(s.ev, d2h_));
-      s.draining.store(true);
+      s.drains.store(1);
       const std::size_t k0 = i, k1 = j;
-      pending_.push_back(work_pool().submit([this, &s, dst, &sizes, &off, k0, k1, base] {
+      // one vector per piece: the allocations are spread over the pool
+      pending_.push_back(work_pool().submit([&s, dst, &sizes, &off, k0, k1, base] {
         check(ucg_event_synchronize(s.ev));
         const T* h = static_cast<const T*>(s.buf);
-        for (std::size_t k = k0; k < k1; ++k) (*dst)[k].assign(h + off[k] - base, h + off[k] - base + sizes[k]);
-        s.draining.store(false);
+        constexpr std::size_t kBlk = 2048;
+        work_pool().parallel_for((k1 - k0 + kBlk - 1) / kBlk, [&](std::size_t blk) {
+          const std::size_t e = std::min(k1, k0 + (blk + 1) * kBlk);
+          for (std::size_t k = k0 + blk * kBlk; k < e; ++k)
+            (*dst)[k].assign(h + off[k] - base, h + off[k] - base + sizes[k]);
+        });
+        s.drains.fetch_sub(1);
       }));
       i = j;
     }
@@ -380,7 +392,7 @@ class HostPipe {
     void* buf = nullptr;
     void* ev = nullptr;
     bool busy = false;                 // in ring: an H2D from it may be in flight
-    std::atomic<bool> draining{false};  // out ring: a drain task still reads it
+    std::atomic<int> drains{0};        // out ring: drain tasks still reading it
   };
   struct Ring {
     Slot slot[kSlots];
@@ -399,7 +411,7 @@ class HostPipe {
   Slot& acquire_out() {
     Slot& s = out_.slot[out_.next];
     out_.next = (out_.next + 1) % kSlots;
-    while (s.draining.load()) std::this_thread::yield();  // its drain task is on the pool
+    while (s.drains.load() > 0) std::this_thread::yield();  // its drain tasks are on the pool
     return s;
   }
 
