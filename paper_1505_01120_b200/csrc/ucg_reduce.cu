@@ -630,12 +630,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   __syncthreads();
   if (ticket + F < G) return;
   if (threadIdx.x == 0) {
-    uint64_t spins = 0;
+    // every CTA is resident (cooperative launch), so the others finish their
+    // stream; a wait of kPeerWaitNs cannot happen — trap rather than reduce
+    // item roots that are not all written
+    const uint64_t t0 = global_ns();
+    uint32_t spins = 0;
     while (ld_acquire_gpu(p.fin.done) < G) {
       __nanosleep(32);
-      if (++spins > (1ull << 25)) {  // cannot happen under a cooperative launch:
-        __trap();                    // never reduce item roots that are not all written
-      }
+      if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();
     }
   }
   __syncthreads();
