@@ -264,6 +264,24 @@ def test_reduce_cl_many_short_elements(cuda, length, op):
     assert np.array_equal(outi.cpu().numpy(), O.reduce_cl(xi.reshape(count, length), counts))
 
 
+@pytest.mark.parametrize("nparts", [4097, 9000])
+def test_reduce_cl_beyond_4096_partitions(cuda, nparts):
+    """Stage 2 over more than 4096 non-empty partitions (no partition limit,
+    as the reference engine.hpp:172-190 has none): one element per partition,
+    so the result is the pairing tree over all of them."""
+    from paper_1505_01120_b200 import ops
+
+    length = 3
+    x = (O.fill_uniform(77, nparts * length) * np.float32(2) - np.float32(1)).astype(np.float32)
+    elems = x.reshape(nparts, length)
+    xd = torch.from_numpy(x).to(cuda)
+    ptrs = torch.tensor([xd.data_ptr() + 4 * length * i for i in range(nparts)], dtype=torch.int64, device=cuda)
+    out = torch.empty(length, dtype=torch.float32, device=cuda)
+    counts = [1] * nparts
+    ops.reduce_cl_vectors(ptrs, nparts, length, counts, "sum", out)
+    assert np.array_equal(_bits(out), O.reduce_cl(elems, counts, "sum").view(np.uint32))
+
+
 def test_reduce_cl_isum_golden(cuda, golden):
     from test_oracle_golden import _isum_cases
 
