@@ -357,6 +357,28 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
       : "memory");
 }
 
+// 32 consecutive TMEM columns of this warp's 32 lanes -> r[0..31] (waits)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // kTerms = 1: C = A*B in TF32 (the tensor core reads the top 19 bits of
 // each fp32 operand). kTerms = 3 (fp32-faithful "3xTF32"): the operands are
 // pre-split into x = hi + lo with hi = rna_tf32(x) and lo = x - hi (exact),
@@ -364,8 +386,18 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
 // the same TMEM accumulator — the dropped lo*lo term and lo's own TF32
 // truncation are ~2^-22 relative, fp32-level. tmA/tmB are then Ahi/Bhi and
 // tmA2/tmB2 Alo/Blo.
+// Threads per CTA: warp 0 TMA, warp 1 TMEM alloc + MMA, then the epilogue
+// warps — 4 for TF32 (one per TMEM lane group), 8 for the k-chunked fp32
+// mode (two per lane group, each owning 128 of the tile's 256 columns and
+// keeping that half-row's running chunk sum in registers).
 template <int kTerms>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+constexpr int gemm2_threads() { return kTerms == 1 ? 192 : 320; }
+
+// (__maxnreg__ rather than __launch_bounds__: with the bounds ptxas capped the
+// fp32 mode at 168 registers and spilled the running sums; 200 x 320 threads
+// fits the register file)
+template <int kTerms>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
     k_gemm_tf32_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                     float* __restrict__ C, int n, int nchunks) {
@@ -393,7 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 256);  // both CTAs' 128 epilogue threads
+      mbar_init(&tempty[a], 2 * (gemm2_threads<kTerms>() - 64));  // both CTAs' epilogue threads
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -470,12 +502,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         mma_commit_2sm(&tfull[acc]);
       }
     }
-  } else {
+  } else if constexpr (kTerms == 1) {
     const int lg = warp & 3;
     const uint32_t leader_tempty[2] = {smem_addr(&tempty[0]) & kPeerMask, smem_addr(&tempty[1]) & kPeerMask};
     uint32_t i = 0;
     for (int u = 0; u < ((ntiles - pair + npairs - 1) / npairs) * nchunks; ++u, ++i) {
-      const int t = pair + (u / nchunks) * npairs, chunk = u % nchunks;
+      const int t = pair + (u / nchunks) * npairs;
       int mb, nb;
       {
         const int per_group = kGroupM * tiles_n;
@@ -491,58 +523,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 #pragma unroll 1
       for (int c = 0; c < 256 / 32; ++c) {
         uint32_t r[32];
-        const uint32_t taddr = tmem + (uint32_t(lg * 32) << 16) + acc * 256u + uint32_t(c * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
-              "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-              "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if constexpr (kTerms == 1) {
-          float4* dst = reinterpret_cast<float4*>(crow + c * 32);
+        tmem_ld32(tmem + (uint32_t(lg * 32) << 16) + acc * 256u + uint32_t(c * 32), r);
+        float4* dst = reinterpret_cast<float4*>(crow + c * 32);
 #pragma unroll
-          for (int qq = 0; qq < 8; ++qq)
-            __stcs(dst + qq, make_float4(__uint_as_float(r[4 * qq]), __uint_as_float(r[4 * qq + 1]),
-                                         __uint_as_float(r[4 * qq + 2]), __uint_as_float(r[4 * qq + 3])));
-        } else {
-          // k-chunk units: the warp's 32x32 block goes through shared memory
-          // (rows padded to 33 floats: conflict-free both ways) so C is read
-          // and written a row segment of 128 B per 8 lanes instead of one
-          // 16-byte piece of 32 different rows per instruction; chunk 0
-          // stores, later chunks add (round-to-nearest) to what this warp
-          // stored for the previous chunk.
-          __shared__ float stg[4][32][33];
-          float(*blk)[33] = stg[lg];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) blk[lane][j] = __uint_as_float(r[j]);
-          __syncwarp();
-          const int rq = lane >> 3, cq = (lane & 7) * 4;
-          float* base = C + size_t(mb * 256 + int(rank) * 128 + lg * 32) * n + nb * 256 + c * 32 + cq;
-          float4 o[8];
-          if (chunk > 0) {
-#pragma unroll
-            for (int it = 0; it < 8; ++it) o[it] = __ldcg(reinterpret_cast<const float4*>(base + size_t(it * 4 + rq) * n));
-          }
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int row = it * 4 + rq;
-            float4 v = make_float4(blk[row][cq], blk[row][cq + 1], blk[row][cq + 2], blk[row][cq + 3]);
-            if (chunk > 0)
-              v = make_float4(__fadd_rn(o[it].x, v.x), __fadd_rn(o[it].y, v.y), __fadd_rn(o[it].z, v.z),
-                              __fadd_rn(o[it].w, v.w));
-            float4* dst = reinterpret_cast<float4*>(base + size_t(row) * n);
-            if (chunk + 1 == nchunks) __stcs(dst, v);
-            else __stcg(dst, v);
-          }
-          __syncwarp();
-        }
+        for (int qq = 0; qq < 8; ++qq)
+          __stcs(dst + qq, make_float4(__uint_as_float(r[4 * qq]), __uint_as_float(r[4 * qq + 1]),
+                                       __uint_as_float(r[4 * qq + 2]), __uint_as_float(r[4 * qq + 3])));
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_tempty[acc]) : "memory");
+    }
+  } else {
+    // k-chunk units: chunk c of a tile is accumulated from zero in TMEM (the
+    // tensor core's truncating fp32 accumulation stays short) and added
+    // into a running fp32 sum with IEEE round-to-nearest adds (sum = chunk
+    // 0, then sum = sum + chunk c); the running sum never leaves the
+    // registers of the thread that owns that half-row, and C is written
+    // once per tile. The MMA fills the other TMEM accumulator meanwhile.
+    const int ew = warp - 2, lg = warp & 3, half = ew >> 2;
+    const uint32_t leader_tempty[2] = {smem_addr(&tempty[0]) & kPeerMask, smem_addr(&tempty[1]) & kPeerMask};
+    float sum[128];
+    uint32_t i = 0;
+    for (int u = 0; u < ((ntiles - pair + npairs - 1) / npairs) * nchunks; ++u, ++i) {
+      const int t = pair + (u / nchunks) * npairs, chunk = u % nchunks;
+      const uint32_t acc = i & 1;
+      mbar_wait(&tfull[acc], (i / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[16];
+        tmem_ld16(tmem + (uint32_t(lg * 32) << 16) + acc * 256u + uint32_t(half * 128 + c * 16), r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          sum[c * 16 + j] = chunk ? __fadd_rn(sum[c * 16 + j], __uint_as_float(r[j])) : __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_tempty[acc]) : "memory");
+      if (chunk + 1 == nchunks) {
+        int mb, nb;
+        {
+          const int per_group = kGroupM * tiles_n;
+          const int g = t / per_group, idx = t % per_group;
+          const int gm = min(kGroupM, tiles_m - g * kGroupM);
+          mb = g * kGroupM + idx % gm;
+          nb = idx / gm;
+        }
+        float4* dst = reinterpret_cast<float4*>(C + size_t(mb * 256 + int(rank) * 128 + lg * 32 + lane) * n +
+                                                nb * 256 + half * 128);
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq)
+          __stcs(dst + qq, make_float4(sum[4 * qq], sum[4 * qq + 1], sum[4 * qq + 2], sum[4 * qq + 3]));
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -620,7 +651,8 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
   } else if (variant == 2) {
     const uint64_t ntiles = (n / 256) * (n / 256);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count() / 2))) * 2;
-    k_gemm_tf32_2sm<1><<<grid, 192, SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, tmA, tmB, C, int(n), 1);
+    k_gemm_tf32_2sm<1><<<grid, gemm2_threads<1>(), SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, tmA, tmB, C, int(n),
+                                                                                      1);
   } else {
     const uint64_t ntiles = (n / BM) * (n / BN);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count())));
@@ -666,7 +698,8 @@ extern "C" int ucg_gemm_f32(const float* A, const float* B, float* C, uint64_t n
     int kchunk = 256;
     if (const char* e = getenv("UCG_GEMM_KCHUNK")) kchunk = atoi(e);
     if (kchunk < BK || kchunk % BK || n % uint64_t(kchunk)) kchunk = int(n);
-    k_gemm_tf32_2sm<3><<<grid, 192, SMEM2_BYTES, st>>>(tmAh, tmBh, tmAl, tmBl, C, int(n), int(n / kchunk));
+    k_gemm_tf32_2sm<3><<<grid, gemm2_threads<3>(), SMEM2_BYTES, st>>>(tmAh, tmBh, tmAl, tmBl, C, int(n),
+                                                                     int(n / kchunk));
     UCG_LAUNCHED();
   }
   UCG_CUDA(cudaFreeAsync(w, st));
