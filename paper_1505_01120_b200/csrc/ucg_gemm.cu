@@ -370,6 +370,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -393,11 +399,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 template <int kTerms>
 constexpr int gemm2_threads() { return kTerms == 1 ? 192 : 320; }
 
-// (__maxnreg__ rather than __launch_bounds__: with the bounds ptxas capped the
-// fp32 mode at 168 registers and spilled the running sums; 200 x 320 threads
-// fits the register file)
+// (10 warps: 3 on some SM sub-partitions, so at most 168 registers per
+// thread; the running sums take 128, the TMEM reads go 8 columns at a time)
 template <int kTerms>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2_threads<kTerms>(), 1)
     k_gemm_tf32_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                     float* __restrict__ C, int n, int nchunks) {
@@ -550,12 +555,12 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
       mbar_wait(&tfull[acc], (i / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t r[16];
-        tmem_ld16(tmem + (uint32_t(lg * 32) << 16) + acc * 256u + uint32_t(half * 128 + c * 16), r);
+      for (int c = 0; c < 16; ++c) {
+        uint32_t r[8];
+        tmem_ld8(tmem + (uint32_t(lg * 32) << 16) + acc * 256u + uint32_t(half * 128 + c * 8), r);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          sum[c * 16 + j] = chunk ? __fadd_rn(sum[c * 16 + j], __uint_as_float(r[j])) : __uint_as_float(r[j]);
+        for (int j = 0; j < 8; ++j)
+          sum[c * 8 + j] = chunk ? __fadd_rn(sum[c * 8 + j], __uint_as_float(r[j])) : __uint_as_float(r[j]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(leader_tempty[acc]) : "memory");
