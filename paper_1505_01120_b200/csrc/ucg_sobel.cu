@@ -359,6 +359,174 @@ __global__ void __launch_bounds__(kTmaThreads)
   }
 }
 
+// ---- row-streaming path (default for widths that are multiples of 16) -----------
+// Each warp owns a 512-column segment (16 columns per lane) and walks DOWN a
+// balanced range of output rows, so every input row's terms are computed
+// once (not once per tile as above: 10 input rows per 8 output rows there)
+// and the 3-row window lives in registers. Input rows stream in through a
+// per-warp ring of kRing smem slots filled by 1-D bulk copies
+// (cp.async.bulk, one per row: the segment plus 16 bytes either side, the
+// out-of-image side left zero), each completing on its own mbarrier; lane 0
+// refills a slot as soon as the warp has read it, so kRing-1 rows (~3.5 KB)
+// are in flight per warp with no CTA-wide barrier anywhere. The work split
+// is static: the output rows of all bands, concatenated, divided evenly
+// among the warps of one column segment.
+constexpr int kRowThreads = 128;
+constexpr int kRing = 8;
+constexpr uint32_t kSlot = 544;  // 16 B left pad + 512 B + 16 B right pad
+
+struct SobelRows {
+  uint64_t in_off[kMaxBands];
+  uint64_t out_off[kMaxBands];
+  uint32_t first_row[kMaxBands + 1];  // output rows before band b (prefix sums)
+  uint32_t nbands;
+  uint32_t segs;                      // 512-column segments per row
+  uint32_t mul[3];                    // {1, 2, 0xFFFFFFFF}, opaque to the compiler
+};
+
+__device__ __forceinline__ void bulk_row(uint32_t dst, const uint8_t* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kRowThreads, kMinBlocks)
+    k_sobel_rows(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, const __grid_constant__ SobelRows p,
+                 uint64_t width) {
+  __shared__ __align__(128) uint8_t ring[kRowThreads / 32][kRing][kSlot];
+  __shared__ __align__(8) uint64_t full[kRowThreads / 32][kRing];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t one = p.mul[0], two = p.mul[1], m1 = p.mul[2];
+  uint8_t(*slots)[kSlot] = ring[wib];
+  // zero the pads once: bytes a copy never writes stay zero (image edge)
+  for (int k = 0; k < kRing; ++k)
+    for (uint32_t i = lane * 16; i < kSlot; i += 32 * 16) *reinterpret_cast<uint4*>(&slots[k][i]) = make_uint4(0, 0, 0, 0);
+  if (lane == 0) {
+    for (int k = 0; k < kRing; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[wib][k])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeroed pads before any bulk copy
+  __syncwarp();
+
+  const uint32_t gw = blockIdx.x * (kRowThreads / 32) + wib, nw = gridDim.x * (kRowThreads / 32);
+  const uint32_t seg = gw % p.segs, slot_w = gw / p.segs, nslot = nw / p.segs;
+  if (slot_w >= nslot) return;  // the leftover warps of an uneven split
+  const uint32_t total = p.first_row[p.nbands];
+  const uint32_t g0 = uint32_t(uint64_t(total) * slot_w / nslot), g1 = uint32_t(uint64_t(total) * (slot_w + 1) / nslot);
+  const int64_t c0 = int64_t(seg) * 512;
+  const uint64_t col = uint64_t(c0) + lane * 16;
+  const bool active = col < width;
+  // this warp's copy window in every row: [lo, hi) of the image columns
+  const int64_t lo = c0 - 16 > 0 ? c0 - 16 : 0;
+  const int64_t hi = c0 + 512 + 16 < int64_t(width) ? c0 + 512 + 16 : int64_t(width);
+  const uint32_t bytes = uint32_t(hi - lo), dst_off = uint32_t(lo - (c0 - 16));
+  uint32_t q = 0;  // rows consumed by this warp: row q uses slot q % kRing in phase (q / kRing) & 1
+
+  uint32_t b = 0;
+  {
+    uint32_t l = 0, h = p.nbands;  // band holding output row g0
+    while (h - l > 1) {
+      const uint32_t m = (l + h) >> 1;
+      if (p.first_row[m] <= g0) l = m;
+      else h = m;
+    }
+    b = l;
+  }
+  for (uint32_t g = g0; g < g1; ++b) {
+    const uint32_t r0 = g - p.first_row[b];                  // first local output row of this piece
+    const uint32_t r1 = min(g1, p.first_row[b + 1]) - p.first_row[b];
+    g += r1 - r0;
+    if (r1 <= r0) continue;
+    const uint8_t* src = in + p.in_off[b] + uint64_t(r0) * width + lo;  // input row r0 (the halo above)
+    uint8_t* dst = out + p.out_off[b] + uint64_t(r0) * width + col;
+    const uint32_t nin = r1 - r0 + 2;
+    // prime the ring with this piece's first rows
+    const uint32_t q0 = q;
+    if (lane == 0) {
+      for (uint32_t i = 0; i < min(uint32_t(kRing), nin); ++i) {
+        const uint32_t k = (q0 + i) % kRing;
+        bulk_row(sa(&slots[k][dst_off]), src + uint64_t(i) * width, bytes, sa(&full[wib][k]));
+      }
+    }
+    // input row i -> its terms (waits for its slot, refills the slot with row i + kRing)
+    auto terms = [&](uint32_t i, RowTerms& tr) {
+      const uint32_t k = (q0 + i) % kRing;
+      asm volatile("{\n .reg .pred w;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 w, [%0], %1;\n @!w bra W;\n}\n" ::"r"(
+                       sa(&full[wib][k])), "r"(((q0 + i) / kRing) & 1)
+                   : "memory");
+      const uint32_t row = sa(&slots[k][16 + lane * 16]);
+      uint4 w;
+      uint32_t pw, nw2;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(row));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(row - 4));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw2) : "r"(row + 16));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      uint32_t E[4], O[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        E[kk] = __byte_perm(ws[kk], 0, 0x4240);
+        O[kk] = __byte_perm(ws[kk], 0, 0x4341);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t Le = kk ? __byte_perm(O[kk - 1], O[kk], 0x5432) : __byte_perm(pw, O[0], 0x5453);
+        const uint32_t Ro = kk < 3 ? __byte_perm(E[kk], E[kk + 1], 0x5432) : __byte_perm(E[3], nw2, 0x1432);
+        tr.dh[2 * kk] = mad_u32(Le, m1, O[kk]);
+        tr.dh[2 * kk + 1] = mad_u32(E[kk], m1, Ro);
+        tr.sh[2 * kk] = mad_u32(E[kk], two, mad_u32(Le, one, O[kk]));
+        tr.sh[2 * kk + 1] = mad_u32(O[kk], two, mad_u32(E[kk], one, Ro));
+      }
+      __syncwarp();  // every lane has read slot k
+      if (lane == 0 && i + kRing < nin) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_row(sa(&slots[k][dst_off]), src + uint64_t(i + kRing) * width, bytes, sa(&full[wib][k]));
+      }
+    };
+    auto emit = [&](uint32_t r, const RowTerms& a, const RowTerms& bb, const RowTerms& c) {
+      uint32_t o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t gx = mad_u32(bb.dh[i], two, a.dh[i] + c.dh[i] + 0x04000400u);
+        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;
+        const uint32_t ax = __vmaxu2(gx, mad_u32(gx, m1, 0x08000800u));
+        const uint32_t ay = __vmaxu2(gy, mad_u32(gy, m1, 0x08000800u));
+        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);
+      }
+      if (active) {
+        const uint32_t x0 = __byte_perm(o[0], o[1], 0x6240), x1 = __byte_perm(o[2], o[3], 0x6240);
+        const uint32_t x2 = __byte_perm(o[4], o[5], 0x6240), x3 = __byte_perm(o[6], o[7], 0x6240);
+        st_stream(reinterpret_cast<float4*>(dst + uint64_t(r) * width),
+                  make_float4(__uint_as_float(x0), __uint_as_float(x1), __uint_as_float(x2), __uint_as_float(x3)));
+      }
+    };
+    const uint32_t nrows = r1 - r0;
+    RowTerms t0, t1, t2;
+    terms(0, t0);
+    terms(1, t1);
+    uint32_t r = 0;
+    for (; r + 3 <= nrows; r += 3) {
+      terms(r + 2, t2);
+      emit(r, t0, t1, t2);
+      terms(r + 3, t0);
+      emit(r + 1, t1, t2, t0);
+      terms(r + 4, t1);
+      emit(r + 2, t2, t0, t1);
+    }
+    if (r < nrows) {
+      terms(r + 2, t2);
+      emit(r, t0, t1, t2);
+      if (r + 1 < nrows) {
+        terms(r + 3, t0);
+        emit(r + 1, t1, t2, t0);
+      }
+    }
+    q += nin;
+  }
+}
+
 // Generic path for widths that are not a multiple of 16 (rows not 16-byte
 // aligned): one thread per output pixel, nine byte loads.
 __global__ void __launch_bounds__(256)
@@ -403,7 +571,54 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
   cudaStream_t st = as_stream(stream);
   bool vec = width % 16 == 0 && aligned16(in) && aligned16(out);
   for (uint64_t i = 0; i < nbands && vec; ++i) vec = in_off[i] % 16 == 0 && out_off[i] % 16 == 0;
-  bool tma = vec && width >= 16 && width < (1ull << 31) && !getenv("UCG_SOBEL_NO_TMA");
+  // UCG_SOBEL_VARIANT (A/B runs): 0 = row streaming (default), 1 = TMA tiles,
+  // 2 = register streaming without TMA
+  static const int variant = [] {
+    const char* e = getenv("UCG_SOBEL_VARIANT");
+    return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 0);
+  }();
+  if (vec && variant == 0 && width < (1ull << 31)) {
+    // CTAs per SM the register budget targets (UCG_SOBEL_ROWS_MINB, A/B runs)
+    static const int minb = [] {
+      const char* e = getenv("UCG_SOBEL_ROWS_MINB");
+      const int v = e ? atoi(e) : 5;
+      return (v == 6 || v == 8) ? v : 5;
+    }();
+    auto kern = minb == 8 ? k_sobel_rows<8> : minb == 6 ? k_sobel_rows<6> : k_sobel_rows<5>;
+    static std::atomic<uint64_t> occ_seen{0};
+    static int per_sm = 1;
+    if (first_on_device(occ_seen))
+      UCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0));
+    for (uint64_t b0 = 0; b0 < nbands; b0 += kMaxBands) {
+      const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));
+      SobelRows p;
+      p.nbands = nb;
+      p.segs = uint32_t((width + 511) / 512);
+      p.mul[0] = 1;
+      p.mul[1] = 2;
+      p.mul[2] = 0xFFFFFFFFu;
+      p.first_row[0] = 0;
+      uint64_t tot = 0;
+      for (uint32_t i = 0; i < nb; ++i) {
+        p.in_off[i] = in_off[b0 + i];
+        p.out_off[i] = out_off[b0 + i];
+        tot += rows[b0 + i];
+        if (tot >= (1ull << 32)) return fail(UCG_ERR_ARG, "sobel: more than 2^32 output rows in one launch");
+        p.first_row[i + 1] = uint32_t(tot);
+      }
+      if (!tot) continue;
+      // every resident warp streams; a column segment's warps split its rows
+      // evenly, at least 8 rows each so a band's halo overhead stays small
+      const uint64_t warps_fill = uint64_t(sm_count()) * std::max(1, per_sm) * (kRowThreads / 32);
+      const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(warps_fill / p.segs, (tot + 7) / 8));
+      const uint64_t warps = per_seg * p.segs;
+      const unsigned grid = unsigned((warps + kRowThreads / 32 - 1) / (kRowThreads / 32));
+      kern<<<grid, kRowThreads, 0, st>>>(in, out, p, width);
+      UCG_LAUNCHED();
+    }
+    return UCG_OK;
+  }
+  bool tma = vec && width >= 16 && width < (1ull << 31) && variant == 1;
   uint64_t total_rows = 0;
   for (uint64_t i = 0; i < nbands && tma; ++i) {
     tma = in_off[i] % width == 0 && rows[i] < (1u << 30);
