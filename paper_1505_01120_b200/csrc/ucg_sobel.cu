@@ -362,21 +362,23 @@ __global__ void __launch_bounds__(kTmaThreads)
 // ---- row-streaming path (default for widths that are multiples of 16) -----------
 // Each warp owns a 512-column segment (16 columns per lane) and walks DOWN a
 // balanced range of output rows, so every input row's terms are computed
-// once (not once per tile as above: 10 input rows per 8 output rows there)
-// and the 3-row window lives in registers. Input rows stream in through a
-// per-warp ring of kRing smem slots filled by 1-D bulk copies
-// (cp.async.bulk, one per row: the segment plus 16 bytes either side, the
-// out-of-image side left zero), each completing on its own mbarrier; lane 0
-// refills a slot as soon as the warp has read it, so kRing-1 rows (~3.5 KB)
-// are in flight per warp with no CTA-wide barrier anywhere. The work split
-// is static: the output rows of all bands, concatenated, divided evenly
-// among the warps of one column segment.
+// once (the tiled kernel above computes 10 input rows' terms per 8 output
+// rows) and the 3-row window lives in registers. Input rows stream in through
+// a per-warp ring of kSlots smem slots of 3 rows each, filled by 1-D bulk
+// copies (cp.async.bulk, one per row: the segment plus 16 bytes either side,
+// the out-of-image side left zero) completing on the slot's mbarrier; lane 0
+// refills a slot as soon as the warp has read it. One wait and one refill per
+// 3 rows, and the 3-row groups line up with the register window's rotation,
+// so the loop body is straight-line code. No CTA-wide barrier anywhere. The
+// work split is static: the output rows of all bands, concatenated, divided
+// evenly among the warps of one column segment.
 constexpr int kRowThreads = 128;
-constexpr int kRing = 8;
-constexpr uint32_t kSlot = 544;  // 16 B left pad + 512 B + 16 B right pad
+constexpr uint32_t kRowBytes = 544;  // 16 B left pad + 512 B + 16 B right pad
+constexpr uint32_t kBoxBytes = 3 * kRowBytes;  // one TMA box: 3 rows
+constexpr uint32_t kGroupBytes = 1664;         // slot stride: the box rounded up to 128 B (TMA alignment)
 
 struct SobelRows {
-  uint64_t in_off[kMaxBands];
+  uint32_t in_row0[kMaxBands];        // first input row of band b in the 2-D view of the input
   uint64_t out_off[kMaxBands];
   uint32_t first_row[kMaxBands + 1];  // output rows before band b (prefix sums)
   uint32_t nbands;
@@ -384,31 +386,24 @@ struct SobelRows {
   uint32_t mul[3];                    // {1, 2, 0xFFFFFFFF}, opaque to the compiler
 };
 
-__device__ __forceinline__ void bulk_row(uint32_t dst, const uint8_t* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-
-template <int kMinBlocks>
+template <int kMinBlocks, int kSlots>
 __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
-    k_sobel_rows(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, const __grid_constant__ SobelRows p,
-                 uint64_t width) {
-  __shared__ __align__(128) uint8_t ring[kRowThreads / 32][kRing][kSlot];
-  __shared__ __align__(8) uint64_t full[kRowThreads / 32][kRing];
+    k_sobel_rows(const __grid_constant__ CUtensorMap rows3, uint8_t* __restrict__ out,
+                 const __grid_constant__ SobelRows p, uint64_t width) {
+  extern __shared__ __align__(128) uint8_t dyn[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t one = p.mul[0], two = p.mul[1], m1 = p.mul[2];
-  uint8_t(*slots)[kSlot] = ring[wib];
-  // zero the pads once: bytes a copy never writes stay zero (image edge)
-  for (int k = 0; k < kRing; ++k)
-    for (uint32_t i = lane * 16; i < kSlot; i += 32 * 16) *reinterpret_cast<uint4*>(&slots[k][i]) = make_uint4(0, 0, 0, 0);
+  uint8_t* ring = dyn + wib * (kSlots * kGroupBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (kRowThreads / 32) * kSlots * kGroupBytes) + wib * kSlots;
+  // zero the ring once: bytes a copy never writes (the out-of-image pads)
+  // stay zero
+  for (uint32_t i = lane * 16; i < kSlots * kGroupBytes; i += 32 * 16)
+    *reinterpret_cast<uint4*>(ring + i) = make_uint4(0, 0, 0, 0);
   if (lane == 0) {
-    for (int k = 0; k < kRing; ++k)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[wib][k])));
+    for (int k = 0; k < kSlots; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeroed pads before any bulk copy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeroes before any bulk copy
   __syncwarp();
 
   const uint32_t gw = blockIdx.x * (kRowThreads / 32) + wib, nw = gridDim.x * (kRowThreads / 32);
@@ -419,11 +414,10 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
   const int64_t c0 = int64_t(seg) * 512;
   const uint64_t col = uint64_t(c0) + lane * 16;
   const bool active = col < width;
-  // this warp's copy window in every row: [lo, hi) of the image columns
-  const int64_t lo = c0 - 16 > 0 ? c0 - 16 : 0;
-  const int64_t hi = c0 + 512 + 16 < int64_t(width) ? c0 + 512 + 16 : int64_t(width);
-  const uint32_t bytes = uint32_t(hi - lo), dst_off = uint32_t(lo - (c0 - 16));
-  uint32_t q = 0;  // rows consumed by this warp: row q uses slot q % kRing in phase (q / kRing) & 1
+  // this warp's window in every row: image columns [c0 - 16, c0 + 528) as 68
+  // 8-byte elements; the parts outside the image are zero-filled by the TMA
+  const int x8 = int(c0 / 8) - 2;
+  uint32_t q = 0;  // row groups consumed by this warp: group q uses slot q % kSlots, phase (q / kSlots) & 1
 
   uint32_t b = 0;
   {
@@ -436,33 +430,35 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
     b = l;
   }
   for (uint32_t g = g0; g < g1; ++b) {
-    const uint32_t r0 = g - p.first_row[b];                  // first local output row of this piece
+    const uint32_t r0 = g - p.first_row[b];  // first local output row of this piece
     const uint32_t r1 = min(g1, p.first_row[b + 1]) - p.first_row[b];
     g += r1 - r0;
     if (r1 <= r0) continue;
-    const uint8_t* src = in + p.in_off[b] + uint64_t(r0) * width + lo;  // input row r0 (the halo above)
+    const int y0 = int(p.in_row0[b] + r0);  // input row r0 of the band (the halo above output row r0)
     uint8_t* dst = out + p.out_off[b] + uint64_t(r0) * width + col;
-    const uint32_t nin = r1 - r0 + 2;
-    // prime the ring with this piece's first rows
-    const uint32_t q0 = q;
-    if (lane == 0) {
-      for (uint32_t i = 0; i < min(uint32_t(kRing), nin); ++i) {
-        const uint32_t k = (q0 + i) % kRing;
-        bulk_row(sa(&slots[k][dst_off]), src + uint64_t(i) * width, bytes, sa(&full[wib][k]));
-      }
-    }
-    // input row i -> its terms (waits for its slot, refills the slot with row i + kRing)
-    auto terms = [&](uint32_t i, RowTerms& tr) {
-      const uint32_t k = (q0 + i) % kRing;
-      asm volatile("{\n .reg .pred w;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 w, [%0], %1;\n @!w bra W;\n}\n" ::"r"(
-                       sa(&full[wib][k])), "r"(((q0 + i) / kRing) & 1)
-                   : "memory");
-      const uint32_t row = sa(&slots[k][16 + lane * 16]);
+    const uint32_t nin = r1 - r0 + 2, ngroups = (nin + 2) / 3;
+    // lane 0: input rows 3j..3j+2 of this piece into slot (q + j) % kSlots —
+    // one 2-D TMA box of 68 x 8 bytes by 3 rows (a last partial group reads
+    // rows past the piece: in the 2-D view those are the next band's rows or
+    // zero fill, and the warp never uses them)
+    auto fill = [&](uint32_t j) {
+      const uint32_t k = (q + j) % kSlots;
+      const uint32_t bar = sa(&full[k]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBoxBytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              sa(ring + k * kGroupBytes)),
+          "l"(&rows3), "r"(x8), "r"(y0 + int(3 * j)), "r"(bar)
+          : "memory");
+    };
+    if (lane == 0)
+      for (uint32_t j = 0; j < min(uint32_t(kSlots), ngroups); ++j) fill(j);
+    auto terms = [&](uint32_t row_s, RowTerms& tr) {
       uint4 w;
       uint32_t pw, nw2;
-      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(row));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(row - 4));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw2) : "r"(row + 16));
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(row_s));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(row_s - 4));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw2) : "r"(row_s + 16));
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
       uint32_t E[4], O[4];
 #pragma unroll
@@ -478,11 +474,6 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
         tr.dh[2 * kk + 1] = mad_u32(E[kk], m1, Ro);
         tr.sh[2 * kk] = mad_u32(E[kk], two, mad_u32(Le, one, O[kk]));
         tr.sh[2 * kk + 1] = mad_u32(O[kk], two, mad_u32(E[kk], one, Ro));
-      }
-      __syncwarp();  // every lane has read slot k
-      if (lane == 0 && i + kRing < nin) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bulk_row(sa(&slots[k][dst_off]), src + uint64_t(i + kRing) * width, bytes, sa(&full[wib][k]));
       }
     };
     auto emit = [&](uint32_t r, const RowTerms& a, const RowTerms& bb, const RowTerms& c) {
@@ -502,29 +493,39 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
                   make_float4(__uint_as_float(x0), __uint_as_float(x1), __uint_as_float(x2), __uint_as_float(x3)));
       }
     };
-    const uint32_t nrows = r1 - r0;
+    // group j = input rows 3j, 3j+1, 3j+2 -> window slots t0, t1, t2 (output
+    // row i-2 needs input rows i-2, i-1, i)
     RowTerms t0, t1, t2;
-    terms(0, t0);
-    terms(1, t1);
-    uint32_t r = 0;
-    for (; r + 3 <= nrows; r += 3) {
-      terms(r + 2, t2);
-      emit(r, t0, t1, t2);
-      terms(r + 3, t0);
-      emit(r + 1, t1, t2, t0);
-      terms(r + 4, t1);
-      emit(r + 2, t2, t0, t1);
-    }
-    if (r < nrows) {
-      terms(r + 2, t2);
-      emit(r, t0, t1, t2);
-      if (r + 1 < nrows) {
-        terms(r + 3, t0);
-        emit(r + 1, t1, t2, t0);
+    for (uint32_t j = 0; j < ngroups; ++j) {
+      const uint32_t k = (q + j) % kSlots;
+      asm volatile("{\n .reg .pred w;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 w, [%0], %1;\n @!w bra W;\n}\n" ::"r"(
+                       sa(&full[k])), "r"(((q + j) / kSlots) & 1)
+                   : "memory");
+      const uint32_t base = sa(ring + k * kGroupBytes + 16 + lane * 16);
+      const uint32_t i0 = 3 * j;
+      terms(base, t0);
+      if (i0 >= 2) emit(i0 - 2, t1, t2, t0);
+      if (i0 + 1 < nin) {
+        terms(base + kRowBytes, t1);
+        if (i0 + 1 >= 2) emit(i0 - 1, t2, t0, t1);
+        if (i0 + 2 < nin) {
+          terms(base + 2 * kRowBytes, t2);
+          emit(i0, t0, t1, t2);
+        }
+      }
+      __syncwarp();  // every lane has read slot k
+      if (lane == 0 && j + kSlots < ngroups) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fill(j + kSlots);
       }
     }
-    q += nin;
+    q += ngroups;
   }
+}
+
+template <int kMinBlocks, int kSlots>
+constexpr uint32_t sobel_rows_smem() {
+  return (kRowThreads / 32) * kSlots * (kGroupBytes + 8) + 128;
 }
 
 // Generic path for widths that are not a multiple of 16 (rows not 16-byte
@@ -577,30 +578,58 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
     const char* e = getenv("UCG_SOBEL_VARIANT");
     return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 0);
   }();
-  if (vec && variant == 0 && width < (1ull << 31)) {
+  bool rows_ok = vec && variant == 0 && width < (1ull << 31);
+  for (uint64_t i = 0; i < nbands && rows_ok; ++i) rows_ok = in_off[i] % width == 0;
+  if (rows_ok) {
     // CTAs per SM the register budget targets (UCG_SOBEL_ROWS_MINB, A/B runs)
     static const int minb = [] {
       const char* e = getenv("UCG_SOBEL_ROWS_MINB");
       const int v = e ? atoi(e) : 5;
       return (v == 6 || v == 8) ? v : 5;
     }();
-    auto kern = minb == 8 ? k_sobel_rows<8> : minb == 6 ? k_sobel_rows<6> : k_sobel_rows<5>;
+    static const int slots = [] {
+      const char* e = getenv("UCG_SOBEL_SLOTS");
+      return e && atoi(e) == 6 ? 6 : 4;
+    }();
+    auto kern = slots == 6 ? (minb == 6 ? k_sobel_rows<6, 6> : k_sobel_rows<5, 6>)
+                           : (minb == 6 ? k_sobel_rows<6, 4> : minb == 8 ? k_sobel_rows<8, 4> : k_sobel_rows<5, 4>);
+    const uint32_t smem = slots == 6 ? sobel_rows_smem<5, 6>() : sobel_rows_smem<5, 4>();
     static std::atomic<uint64_t> occ_seen{0};
     static int per_sm = 1;
-    if (first_on_device(occ_seen))
-      UCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, 0));
+    if (first_on_device(occ_seen)) {
+      UCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      UCG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads, smem));
+    }
     for (uint64_t b0 = 0; b0 < nbands; b0 += kMaxBands) {
       const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));
       SobelRows p;
       p.nbands = nb;
       p.segs = uint32_t((width + 511) / 512);
+      uint64_t in_rows = 0;
+      for (uint32_t i = 0; i < nb; ++i) {
+        if (in_off[b0 + i] % width) return fail(UCG_ERR_ARG, "sobel: bands must start on a row boundary");
+        p.in_row0[i] = uint32_t(in_off[b0 + i] / width);
+        in_rows = std::max<uint64_t>(in_rows, in_off[b0 + i] / width + rows[b0 + i] + 2);
+      }
+      if (in_rows >= (1ull << 31)) return fail(UCG_ERR_ARG, "sobel: input too tall for a tensor map");
+      CUtensorMap rows3;
+      {
+        auto enc = tmap_encode_fn();
+        if (!enc) return fail(UCG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        cuuint64_t dims[2] = {width / 8, in_rows};
+        cuuint64_t strides[1] = {width};
+        cuuint32_t box[2] = {kRowBytes / 8, 3}, estr[2] = {1, 1};
+        if (enc(&rows3, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(in), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return fail(UCG_ERR_CUDA, "sobel rows tensor map encode failed");
+      }
       p.mul[0] = 1;
       p.mul[1] = 2;
       p.mul[2] = 0xFFFFFFFFu;
       p.first_row[0] = 0;
       uint64_t tot = 0;
       for (uint32_t i = 0; i < nb; ++i) {
-        p.in_off[i] = in_off[b0 + i];
         p.out_off[i] = out_off[b0 + i];
         tot += rows[b0 + i];
         if (tot >= (1ull << 32)) return fail(UCG_ERR_ARG, "sobel: more than 2^32 output rows in one launch");
@@ -613,7 +642,7 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       const uint64_t per_seg = std::max<uint64_t>(1, std::min<uint64_t>(warps_fill / p.segs, (tot + 7) / 8));
       const uint64_t warps = per_seg * p.segs;
       const unsigned grid = unsigned((warps + kRowThreads / 32 - 1) / (kRowThreads / 32));
-      kern<<<grid, kRowThreads, 0, st>>>(in, out, p, width);
+      kern<<<grid, kRowThreads, smem, st>>>(rows3, out, p, width);
       UCG_LAUNCHED();
     }
     return UCG_OK;
