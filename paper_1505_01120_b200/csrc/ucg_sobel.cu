@@ -572,11 +572,12 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
   cudaStream_t st = as_stream(stream);
   bool vec = width % 16 == 0 && aligned16(in) && aligned16(out);
   for (uint64_t i = 0; i < nbands && vec; ++i) vec = in_off[i] % 16 == 0 && out_off[i] % 16 == 0;
-  // UCG_SOBEL_VARIANT (A/B runs): 0 = row streaming (default), 1 = TMA tiles,
-  // 2 = register streaming without TMA
+  // UCG_SOBEL_VARIANT (A/B runs): 1 = TMA tiles (default), 0 = row streaming
+  // (measured equal: 100.8 vs 99.9 us at 16384^2 — both ALU-pipe bound, see
+  // DESIGN.md §5), 2 = register streaming without TMA
   static const int variant = [] {
     const char* e = getenv("UCG_SOBEL_VARIANT");
-    return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 0);
+    return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 1);
   }();
   bool rows_ok = vec && variant == 0 && width < (1ull << 31);
   for (uint64_t i = 0; i < nbands && rows_ok; ++i) rows_ok = in_off[i] % width == 0;
