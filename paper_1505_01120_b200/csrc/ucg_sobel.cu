@@ -373,37 +373,48 @@ __global__ void __launch_bounds__(kTmaThreads)
 // work split is static: the output rows of all bands, concatenated, divided
 // evenly among the warps of one column segment.
 constexpr int kRowThreads = 128;
-constexpr uint32_t kRowBytes = 544;  // 16 B left pad + 512 B + 16 B right pad
-constexpr uint32_t kBoxBytes = 3 * kRowBytes;  // one TMA box: 3 rows
-constexpr uint32_t kGroupBytes = 1664;         // slot stride: the box rounded up to 128 B (TMA alignment)
+
+// Geometry of a lane owning kCols columns (16 or 8): a warp segment is
+// 32 * kCols columns, a ring row holds it plus 16 bytes either side, a TMA
+// box is 3 such rows, a slot is the box rounded up to 128 bytes.
+template <int kCols>
+struct RowGeom {
+  static constexpr uint32_t seg = 32 * kCols;
+  static constexpr uint32_t row_bytes = seg + 32;
+  static constexpr uint32_t box_bytes = 3 * row_bytes;
+  static constexpr uint32_t slot_bytes = (box_bytes + 127) / 128 * 128;
+};
+
+template <int kW>  // kW 4-byte words = 4 kW pixels per lane
+struct RowTermsW {
+  uint32_t dh[2 * kW];
+  uint32_t sh[2 * kW];
+};
 
 struct SobelRows {
   uint32_t in_row0[kMaxBands];        // first input row of band b in the 2-D view of the input
   uint64_t out_off[kMaxBands];
   uint32_t first_row[kMaxBands + 1];  // output rows before band b (prefix sums)
   uint32_t nbands;
-  uint32_t segs;                      // 512-column segments per row
+  uint32_t segs;                      // column segments per row
   uint32_t mul[3];                    // {1, 2, 0xFFFFFFFF}, opaque to the compiler
 };
 
-template <int kMinBlocks, int kSlots>
+template <int kMinBlocks, int kSlots, int kCols>
 __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
     k_sobel_rows(const __grid_constant__ CUtensorMap rows3, uint8_t* __restrict__ out,
                  const __grid_constant__ SobelRows p, uint64_t width) {
+  using G = RowGeom<kCols>;
+  constexpr int kW = kCols / 4;
   extern __shared__ __align__(128) uint8_t dyn[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t one = p.mul[0], two = p.mul[1], m1 = p.mul[2];
-  uint8_t* ring = dyn + wib * (kSlots * kGroupBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (kRowThreads / 32) * kSlots * kGroupBytes) + wib * kSlots;
-  // zero the ring once: bytes a copy never writes (the out-of-image pads)
-  // stay zero
-  for (uint32_t i = lane * 16; i < kSlots * kGroupBytes; i += 32 * 16)
-    *reinterpret_cast<uint4*>(ring + i) = make_uint4(0, 0, 0, 0);
+  uint8_t* ring = dyn + wib * (kSlots * G::slot_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dyn + (kRowThreads / 32) * kSlots * G::slot_bytes) + wib * kSlots;
   if (lane == 0) {
     for (int k = 0; k < kSlots; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeroes before any bulk copy
   __syncwarp();
 
   const uint32_t gw = blockIdx.x * (kRowThreads / 32) + wib, nw = gridDim.x * (kRowThreads / 32);
@@ -411,11 +422,11 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
   if (slot_w >= nslot) return;  // the leftover warps of an uneven split
   const uint32_t total = p.first_row[p.nbands];
   const uint32_t g0 = uint32_t(uint64_t(total) * slot_w / nslot), g1 = uint32_t(uint64_t(total) * (slot_w + 1) / nslot);
-  const int64_t c0 = int64_t(seg) * 512;
-  const uint64_t col = uint64_t(c0) + lane * 16;
+  const int64_t c0 = int64_t(seg) * G::seg;
+  const uint64_t col = uint64_t(c0) + lane * kCols;
   const bool active = col < width;
-  // this warp's window in every row: image columns [c0 - 16, c0 + 528) as 68
-  // 8-byte elements; the parts outside the image are zero-filled by the TMA
+  // this warp's window in every row: image columns [c0 - 16, c0 + seg + 16)
+  // as 8-byte elements; the parts outside the image are zero-filled by the TMA
   const int x8 = int(c0 / 8) - 2;
   uint32_t q = 0;  // row groups consumed by this warp: group q uses slot q % kSlots, phase (q / kSlots) & 1
 
@@ -438,48 +449,50 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
     uint8_t* dst = out + p.out_off[b] + uint64_t(r0) * width + col;
     const uint32_t nin = r1 - r0 + 2, ngroups = (nin + 2) / 3;
     // lane 0: input rows 3j..3j+2 of this piece into slot (q + j) % kSlots —
-    // one 2-D TMA box of 68 x 8 bytes by 3 rows (a last partial group reads
-    // rows past the piece: in the 2-D view those are the next band's rows or
-    // zero fill, and the warp never uses them)
+    // one 2-D TMA box (a last partial group reads rows past the piece: in the
+    // 2-D view those are the next band's rows or zero fill, never used)
     auto fill = [&](uint32_t j) {
       const uint32_t k = (q + j) % kSlots;
       const uint32_t bar = sa(&full[k]);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBoxBytes) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(G::box_bytes) : "memory");
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-              sa(ring + k * kGroupBytes)),
+              sa(ring + k * G::slot_bytes)),
           "l"(&rows3), "r"(x8), "r"(y0 + int(3 * j)), "r"(bar)
           : "memory");
     };
     if (lane == 0)
       for (uint32_t j = 0; j < min(uint32_t(kSlots), ngroups); ++j) fill(j);
-    auto terms = [&](uint32_t row_s, RowTerms& tr) {
-      uint4 w;
+    auto terms = [&](uint32_t row_s, RowTermsW<kW>& tr) {
+      uint32_t ws[kW];
       uint32_t pw, nw2;
-      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(row_s));
+      if constexpr (kW == 4) {
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(ws[0]), "=r"(ws[1]), "=r"(ws[2]), "=r"(ws[3]) : "r"(row_s));
+      } else {
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(ws[0]), "=r"(ws[1]) : "r"(row_s));
+      }
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(row_s - 4));
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw2) : "r"(row_s + 16));
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-      uint32_t E[4], O[4];
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nw2) : "r"(row_s + 4 * kW));
+      uint32_t E[kW], O[kW];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < kW; ++kk) {
         E[kk] = __byte_perm(ws[kk], 0, 0x4240);
         O[kk] = __byte_perm(ws[kk], 0, 0x4341);
       }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < kW; ++kk) {
         const uint32_t Le = kk ? __byte_perm(O[kk - 1], O[kk], 0x5432) : __byte_perm(pw, O[0], 0x5453);
-        const uint32_t Ro = kk < 3 ? __byte_perm(E[kk], E[kk + 1], 0x5432) : __byte_perm(E[3], nw2, 0x1432);
+        const uint32_t Ro = kk < kW - 1 ? __byte_perm(E[kk], E[kk + 1], 0x5432) : __byte_perm(E[kW - 1], nw2, 0x1432);
         tr.dh[2 * kk] = mad_u32(Le, m1, O[kk]);
         tr.dh[2 * kk + 1] = mad_u32(E[kk], m1, Ro);
         tr.sh[2 * kk] = mad_u32(E[kk], two, mad_u32(Le, one, O[kk]));
         tr.sh[2 * kk + 1] = mad_u32(O[kk], two, mad_u32(E[kk], one, Ro));
       }
     };
-    auto emit = [&](uint32_t r, const RowTerms& a, const RowTerms& bb, const RowTerms& c) {
-      uint32_t o[8];
+    auto emit = [&](uint32_t r, const RowTermsW<kW>& a, const RowTermsW<kW>& bb, const RowTermsW<kW>& c) {
+      uint32_t o[2 * kW];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 2 * kW; ++i) {
         const uint32_t gx = mad_u32(bb.dh[i], two, a.dh[i] + c.dh[i] + 0x04000400u);
         const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;
         const uint32_t ax = __vmaxu2(gx, mad_u32(gx, m1, 0x08000800u));
@@ -487,29 +500,34 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
         o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);
       }
       if (active) {
-        const uint32_t x0 = __byte_perm(o[0], o[1], 0x6240), x1 = __byte_perm(o[2], o[3], 0x6240);
-        const uint32_t x2 = __byte_perm(o[4], o[5], 0x6240), x3 = __byte_perm(o[6], o[7], 0x6240);
-        st_stream(reinterpret_cast<float4*>(dst + uint64_t(r) * width),
-                  make_float4(__uint_as_float(x0), __uint_as_float(x1), __uint_as_float(x2), __uint_as_float(x3)));
+        uint32_t x[kW];
+#pragma unroll
+        for (int kk = 0; kk < kW; ++kk) x[kk] = __byte_perm(o[2 * kk], o[2 * kk + 1], 0x6240);
+        if constexpr (kW == 4) {
+          st_stream(reinterpret_cast<float4*>(dst + uint64_t(r) * width),
+                    make_float4(__uint_as_float(x[0]), __uint_as_float(x[1]), __uint_as_float(x[2]), __uint_as_float(x[3])));
+        } else {
+          __stcs(reinterpret_cast<uint2*>(dst + uint64_t(r) * width), make_uint2(x[0], x[1]));
+        }
       }
     };
     // group j = input rows 3j, 3j+1, 3j+2 -> window slots t0, t1, t2 (output
     // row i-2 needs input rows i-2, i-1, i)
-    RowTerms t0, t1, t2;
+    RowTermsW<kW> t0, t1, t2;
     for (uint32_t j = 0; j < ngroups; ++j) {
       const uint32_t k = (q + j) % kSlots;
       asm volatile("{\n .reg .pred w;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 w, [%0], %1;\n @!w bra W;\n}\n" ::"r"(
                        sa(&full[k])), "r"(((q + j) / kSlots) & 1)
                    : "memory");
-      const uint32_t base = sa(ring + k * kGroupBytes + 16 + lane * 16);
+      const uint32_t base = sa(ring + k * G::slot_bytes + 16 + lane * kCols);
       const uint32_t i0 = 3 * j;
       terms(base, t0);
       if (i0 >= 2) emit(i0 - 2, t1, t2, t0);
       if (i0 + 1 < nin) {
-        terms(base + kRowBytes, t1);
+        terms(base + G::row_bytes, t1);
         if (i0 + 1 >= 2) emit(i0 - 1, t2, t0, t1);
         if (i0 + 2 < nin) {
-          terms(base + 2 * kRowBytes, t2);
+          terms(base + 2 * G::row_bytes, t2);
           emit(i0, t0, t1, t2);
         }
       }
@@ -523,9 +541,9 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
   }
 }
 
-template <int kMinBlocks, int kSlots>
+template <int kSlots, int kCols>
 constexpr uint32_t sobel_rows_smem() {
-  return (kRowThreads / 32) * kSlots * (kGroupBytes + 8) + 128;
+  return (kRowThreads / 32) * kSlots * (RowGeom<kCols>::slot_bytes + 8) + 128;
 }
 
 // Generic path for widths that are not a multiple of 16 (rows not 16-byte
@@ -582,19 +600,21 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
   bool rows_ok = vec && variant == 0 && width < (1ull << 31);
   for (uint64_t i = 0; i < nbands && rows_ok; ++i) rows_ok = in_off[i] % width == 0;
   if (rows_ok) {
-    // CTAs per SM the register budget targets (UCG_SOBEL_ROWS_MINB, A/B runs)
-    static const int minb = [] {
-      const char* e = getenv("UCG_SOBEL_ROWS_MINB");
-      const int v = e ? atoi(e) : 5;
-      return (v == 6 || v == 8) ? v : 5;
+    // A/B knobs: UCG_SOBEL_COLS (columns per lane, 16 or 8), UCG_SOBEL_SLOTS
+    // (3-row slots per warp, 4 or 6)
+    static const int cols = [] {
+      const char* e = getenv("UCG_SOBEL_COLS");
+      return e && atoi(e) == 8 ? 8 : 16;
     }();
     static const int slots = [] {
       const char* e = getenv("UCG_SOBEL_SLOTS");
       return e && atoi(e) == 6 ? 6 : 4;
     }();
-    auto kern = slots == 6 ? (minb == 6 ? k_sobel_rows<6, 6> : k_sobel_rows<5, 6>)
-                           : (minb == 6 ? k_sobel_rows<6, 4> : minb == 8 ? k_sobel_rows<8, 4> : k_sobel_rows<5, 4>);
-    const uint32_t smem = slots == 6 ? sobel_rows_smem<5, 6>() : sobel_rows_smem<5, 4>();
+    auto kern = cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16> : k_sobel_rows<5, 4, 16>)
+                           : (slots == 6 ? k_sobel_rows<8, 6, 8> : k_sobel_rows<8, 4, 8>);
+    const uint32_t smem = cols == 16 ? (slots == 6 ? sobel_rows_smem<6, 16>() : sobel_rows_smem<4, 16>())
+                                     : (slots == 6 ? sobel_rows_smem<6, 8>() : sobel_rows_smem<4, 8>());
+    const uint32_t seg_cols = 32u * uint32_t(cols);
     static std::atomic<uint64_t> occ_seen{0};
     static int per_sm = 1;
     if (first_on_device(occ_seen)) {
@@ -605,7 +625,7 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));
       SobelRows p;
       p.nbands = nb;
-      p.segs = uint32_t((width + 511) / 512);
+      p.segs = uint32_t((width + seg_cols - 1) / seg_cols);
       uint64_t in_rows = 0;
       for (uint32_t i = 0; i < nb; ++i) {
         if (in_off[b0 + i] % width) return fail(UCG_ERR_ARG, "sobel: bands must start on a row boundary");
@@ -619,7 +639,7 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
         if (!enc) return fail(UCG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
         cuuint64_t dims[2] = {width / 8, in_rows};
         cuuint64_t strides[1] = {width};
-        cuuint32_t box[2] = {kRowBytes / 8, 3}, estr[2] = {1, 1};
+        cuuint32_t box[2] = {(seg_cols + 32) / 8, 3}, estr[2] = {1, 1};
         if (enc(&rows3, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(in), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
