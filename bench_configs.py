@@ -56,6 +56,13 @@ def _ref_workload(argv, timeout=900):
     return json.loads(out.strip().splitlines()[-1])
 
 
+def _traffic(key: str, share: float):
+    """ncu DRAM bytes of one full-size launch (profiles/ncu_summary.json),
+    scaled to this rank's share of the units; None when not captured."""
+    v = B.load_traffic(key)
+    return None if v is None else int(v * share)
+
+
 def _line(args, world, workload, metric_desc, value, unit, step_ms, launches, clk, e2e, roofline, cpu, config):
     return {"metric": f"{B.METRIC} [{workload}: {metric_desc}]", "value": value, "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
@@ -225,8 +232,8 @@ def run(args, world, rank, local):
                      {"value": H * W / (e2e_ms * 1e-3), "unit": "pixels/s",
                       "h2d_bytes_per_step": nb * (R + 2) * W, "d2h_bytes_per_step": H * W},
                      {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
-                      "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
-                      "algorithmic_bytes_per_launch": algo},
+                      "frac": achieved / peak_hbm, "traffic": _traffic("sobel_dram_bytes", ln / nb),
+                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": algo},
                      cpu, {"workload": CONFIGS[3], "height": H, "width": W, "bands": nb, "rows_per_band": R,
                            "dtype": "u8", "l2": "inputs larger than L2 (257 MiB image in, 256 MiB out)"})
     elif args.workload == "c5":
@@ -297,7 +304,9 @@ def run(args, world, rank, local):
                      {"value": flops / (e2e_ms * 1e-3), "unit": "FLOP/s",
                       "h2d_bytes_per_step": P * 2 * n * n * 4, "d2h_bytes_per_step": P * n * n * 4},
                      {"bound": "tensor", "achieved": tc32, "peak": peak, "unit": "TFLOP/s", "frac": tc32 / peak,
-                      "traffic": None, "peak_kind": "cuBLAS TF32 8192^3 measured in this run",
+                      "traffic": _traffic("gemm_f32_dram_bytes", 1.0), "traffic_note": "ncu DRAM bytes of one "
+                      "8192^3 fp32-faithful launch (profiles/ncu_summary.json r02)",
+                      "peak_kind": "cuBLAS TF32 8192^3 measured in this run",
                       "note": "achieved counts the tensor work: 3 TF32 products (Ahi*Bhi, Ahi*Blo, Alo*Bhi) per fp32 "
                               "product; the split pass (0.25 ms, HBM-bound) is inside the timed step"},
                      cpu, {"workload": CONFIGS[4], "n": n, "partitions": P,
@@ -408,8 +417,8 @@ def run(args, world, rank, local):
                      {"value": total / (e2e_ms * 1e-3), "unit": "bytes/s", "h2d_bytes_per_step": total,
                       "d2h_bytes_per_step": total, "note": "text up, flags down (the host tokeniser's input)"},
                      {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
-                      "frac": achieved / peak_hbm, "traffic": None, "peak_kind": peak_kind,
-                      "algorithmic_bytes_per_launch": algo},
+                      "frac": achieved / peak_hbm, "traffic": _traffic("wordflags_dram_bytes", ln / chunks),
+                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": algo},
                      cpu, {"workload": "1 GiB synthetic text in 64 chunks of 16 MiB, word-start flags (u8 per byte)",
                            "bytes": total, "chunks": chunks, "dtype": "u8", "word_starts_this_rank": words,
                            "l2": "inputs larger than L2 (1 GiB text)"})
