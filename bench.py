@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-engine-e2e", action="store_true")
+    ap.add_argument("--no-tuned-heap", action="store_true",
+                    help="skip the seam-A leg in a child process with a warm-heap glibc (and the reference beside it)")
     ap.add_argument("--no-graph", action="store_true", help="launch the K timed steps one by one")
     ap.add_argument("--workload", default="c2", choices=["c1", "c1lit", "c2", "c3", "c4", "c5", "wc"],
                     help="c2 (default) is the headline; the others are the remaining BASELINE configs")
@@ -286,6 +288,44 @@ def reference_parity(args, pipe, result: float) -> dict | None:
             "partials_match": mine == want, "partials_checked": len(mine)}
 
 
+HEAP_TUNABLES = "glibc.malloc.hugetlb=1:glibc.malloc.mmap_max=0:glibc.malloc.trim_threshold=68719476736"
+
+
+def tuned_heap_leg(args) -> dict:
+    """The same seam-A chain in a child process whose glibc keeps a warm heap
+    (no mmap per large block, no trim, transparent huge pages): the
+    reference Engine copies every 4 GiB collection into fresh memory twice
+    per operator, and with the default allocator those copies are bound by
+    page faults. Reported beside the default-process number, together with
+    the reference CPU path under the SAME settings (it speeds up too), so
+    neither side is compared against the other's allocator."""
+    env = dict(os.environ, GLIBC_TUNABLES=HEAP_TUNABLES)
+    out = {"glibc_tunables": HEAP_TUNABLES}
+    try:
+        r = subprocess.run([sys.executable, str(ROOT / "tools" / "seam_a_breakdown.py"), "--parts", str(args.parts),
+                            "--part-len", str(args.part_len), "--reps", "2"], env=env, capture_output=True, text=True,
+                           timeout=600)
+        reps = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+        warm = reps[-1]
+        out.update({"value": args.parts * args.part_len / warm["total_s"], "unit": UNIT,
+                    "seconds": warm["total_s"], "engine_own_s": warm["engine_own_s"],
+                    "note": "second chain of the child process (the first warms its heap); random input, timing only"})
+    except Exception as e:
+        out.update({"value": None, "error": str(e)[:200]})
+    try:
+        if REF_HARNESS.exists():
+            rr = subprocess.run([str(REF_HARNESS), "bench", "--parts", str(args.parts), "--part-len", str(args.part_len),
+                                 "--threads", str(os.cpu_count() or 1), "--steps", "1", "--warmup", "1", "--op", args.op],
+                                env=env, capture_output=True, text=True, timeout=900)
+            j = json.loads(rr.stdout.strip().splitlines()[-1])
+            out["reference_same_tunables"] = {"value": j["elements"] / statistics.fmean(j["step_s"]), "unit": UNIT,
+                                              "seconds": statistics.fmean(j["step_s"]),
+                                              "result_bits": j["result_bits"]}
+    except Exception as e:
+        out["reference_same_tunables"] = {"value": None, "error": str(e)[:200]}
+    return out
+
+
 def load_peak() -> tuple[float, str]:
     try:
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
@@ -464,6 +504,8 @@ def our_arm(args, world, rank, local):
                         "(pinned staging), map_cl/map_cl_partition/reduce_cl in HBM, one Element back",
                 "result_matches": bool(np.float32(r_dev) == np.float32(result))}
             del xs
+            if not args.no_tuned_heap:
+                engine_e2e["tuned_heap"] = tuned_heap_leg(args)
         except Exception as e:  # reported, not hidden
             engine_e2e = {"value": None, "error": str(e)[:300]}
 
