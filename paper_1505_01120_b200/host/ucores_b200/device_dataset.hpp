@@ -232,8 +232,11 @@ class DeviceEngine {
         }
         pipe.upload_pieces(out.data(p), pieces, off);
       }
+      // the GPU's stream waits for the last DMA by event: the first operator
+      // is enqueued while the tail of the upload is still in flight (the
+      // host payloads are already in pinned slots, so the caller may drop
+      // the host Dataset as soon as upload() returns)
       pipe.compute_after_upload();
-      pipe.drain();
     });
     return out;
   }

@@ -54,6 +54,13 @@ class GpuClusterDriver : public ucores::ClusterDriver {
       worker_ids_.push_back("gpu" + std::to_string(g->ordinal()));
       workers_.push_back(std::make_unique<GpuWorkerRuntime>(worker_ids_.back(), registry, ops, g));
     }
+    // bring-up, as a worker's resources exist before its first task: each
+    // GPU's transfer pipeline (pinned slot rings, copy streams) and the host
+    // copy threads
+    if (opt.mode == Mode::Batched) {
+      for (auto& g : gpus_) g->attached<HostPipe>();
+      work_pool();
+    }
   }
 
   std::uint64_t new_job_id() override { return ++job_id_; }
