@@ -2,7 +2,9 @@
 // the unmodified reference Engine driven through the B200 drop-in drivers.
 #include <chrono>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,6 +20,20 @@
 namespace {
 
 thread_local std::string t_err;
+
+// One DeviceEngine per GPU count for the process (a long-lived engine, as a
+// user keeps one): its device block pool and transfer pipes stay warm across
+// calls. Calls are serialised on it.
+std::mutex g_engine_mu;
+ucores_b200::DeviceEngine& device_engine(const ucores_b200::WorkloadParams& p, int gpus) {
+  // never destroyed: the engines live until the process exits (freeing CUDA
+  // resources from a static destructor would race the runtime's teardown)
+  static auto* engines = new std::map<int, ucores_b200::DeviceEngine*>();
+  auto*& e = (*engines)[gpus];
+  if (!e) e = new ucores_b200::DeviceEngine(p, gpus);
+  e->set_params(p);
+  return *e;
+}
 
 template <class Fn>
 int guarded(Fn fn) {
@@ -62,7 +78,8 @@ int ucd_pipeline_f32(const float* x, const uint64_t* part_lens, uint64_t nparts,
     const std::string pk = op == 1 ? "pmax" : "psum", rk = op == 1 ? "max2" : "sum2";
     if (mode == UCD_MODE_DEVICE) {
       // the device-resident engine: one upload, the chain in HBM, one element back
-      DeviceEngine de(p, gpus);
+      std::lock_guard<std::mutex> lk(g_engine_mu);
+      DeviceEngine& de = device_engine(p, gpus);
       std::vector<Partition> parts(nparts);
       std::uint64_t off = 0;
       for (std::uint64_t q = 0; q < nparts; ++q) {
@@ -213,7 +230,8 @@ int ucd_literal_f32(const float* x, uint64_t n, uint64_t nparts, float a, float 
     Element r;
     std::chrono::steady_clock::time_point t0, t1;
     if (mode == UCD_MODE_DEVICE) {
-      DeviceEngine de(p, gpus);
+      std::lock_guard<std::mutex> lk(g_engine_mu);
+      DeviceEngine& de = device_engine(p, gpus);
       t0 = std::chrono::steady_clock::now();
       Dataset d = dataset();
       r = de.reduce_cl(de.map_cl_partition(de.map_cl(de.upload(d), "axpb"), pk), rk);

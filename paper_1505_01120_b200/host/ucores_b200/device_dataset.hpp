@@ -196,6 +196,8 @@ class DeviceEngine {
     work_pool();
   }
   std::size_t gpu_count() const { return gpus_.size(); }
+  /// Kernel parameters for later calls (axpb's a, b; sobel width; matmul n).
+  void set_params(const WorkloadParams& p) { params_ = p; }
 
   /// Host Dataset -> HBM. Each partition must hold one element kind (a
   /// partition's bytes are its concatenation); tables stay on the host.
