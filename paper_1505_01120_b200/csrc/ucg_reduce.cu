@@ -211,14 +211,64 @@ struct TreeSmem {
 // shuffles (lower lane = left operand), thread 0 the last 3 over the warp
 // roots — one barrier per block. Block roots are merged by a binary-counter
 // stack of aligned subtrees and the stack is folded right to left.
+__device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Tagged values (the tagged tail): slot = {tag << 32 | float bits}, written
+// with ONE 64-bit store (single-copy atomic), so a reader that sees this
+// launch's tag has the value — no fence on the writer's side. Each thread
+// loads its 16 slots, then re-polls (with backoff) only the ones whose tag is
+// not this launch's yet.
+__device__ __forceinline__ void load_tagged16(const uint64_t* slots, uint64_t base, uint64_t n, uint32_t tag,
+                                              float (&v)[kTreeVals], float ident) {
+  uint64_t q[kTreeVals];
+  if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(slots + base) & 15) == 0) {
+#pragma unroll
+    for (int k = 0; k < kTreeVals / 2; ++k)
+      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                   : "=l"(q[2 * k]), "=l"(q[2 * k + 1])
+                   : "l"(slots + base + 2 * k)
+                   : "memory");
+  } else {
+#pragma unroll
+    for (int k = 0; k < kTreeVals; ++k) q[k] = base + k < n ? ld_relaxed_gpu_u64(slots + base + k) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kTreeVals; ++k) {
+    if (base + k >= n) {
+      v[k] = ident;
+      continue;
+    }
+    if (uint32_t(q[k] >> 32) != tag) {
+      const uint64_t t0 = global_ns();
+      uint32_t ns = 64;
+      while (uint32_t((q[k] = ld_relaxed_gpu_u64(slots + base + k)) >> 32) != tag) {
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : ns;
+        if (global_ns() - t0 > kPeerWaitNs) __trap();  // a writer of this launch never stored: cannot happen
+      }
+    }
+    v[k] = __uint_as_float(uint32_t(q[k]));
+  }
+}
+
 template <class Op>
-__device__ float cta_tree(const float* __restrict__ vals, uint64_t n, TreeSmem& sm) {
+__device__ float cta_tree(const float* __restrict__ vals, uint64_t n, TreeSmem& sm,
+                          const uint64_t* tagged = nullptr, uint32_t tag = 0) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint64_t nblocks = (n + kTreeBlock - 1) / kTreeBlock;
   for (uint64_t bi = 0; bi < nblocks; ++bi) {
     const uint64_t base = bi * kTreeBlock + kTreeVals * uint64_t(tid);
     float v[kTreeVals];
-    if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(vals + base) & 15) == 0) {
+    if (tagged) {
+      load_tagged16(tagged, base, n, tag, v, Op::identity());
+    } else if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(vals + base) & 15) == 0) {
       // 4 x 16-byte loads (a quarter of the L2 sector requests of scalar loads)
 #pragma unroll
       for (int k = 0; k < kTreeVals / 4; ++k) {
@@ -294,6 +344,14 @@ struct FinishArgs {
                               // values as it computes them (stage 2 only receives)
   float* sub;                 // tapered tail: 4 sub-item roots per item in [taper_first, +ntaper)
   uint64_t taper_first, ntaper;
+  // tagged tail (cooperative multi-finisher CTA-mode launches): item roots
+  // and partition values as {tag, value} slots of the segment table, so the
+  // FIRST F CTAs out of the stream start the partition trees while the last
+  // items are still streaming, with no fence per CTA and no wait for the
+  // grid; null: the ticketed tail (last F CTAs out, after the whole grid)
+  uint64_t* troots;           // [nitems] item slots, then [nseg] partition-value slots
+  uint32_t* tag_ctr;          // launches completed on this table (this launch's tag = *tag_ctr + 1)
+  uint32_t grid;              // CTAs of the launch (the tagged tail's reset waits for all tickets)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -378,7 +436,7 @@ __device__ __forceinline__ void taper_roots(const FinishArgs& p, uint64_t f, uin
 }
 
 template <class Op>
-__device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm) {
+__device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm, uint32_t tag = 0) {
   const bool send = p.world > 1 && p.early_send;
   if (p.warp_mode) {
     const int lane = threadIdx.x & 31;
@@ -403,9 +461,10 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
       taper_roots<Op>(p, f, n, threadIdx.x, blockDim.x);
       __syncthreads();
     }
-    const float r = n ? cta_tree<Op>(p.partial + f, n, sm) : Op::empty();
+    const float r = n ? cta_tree<Op>(p.partial + f, n, sm, p.troots ? p.troots + f : nullptr, tag) : Op::empty();
     if (threadIdx.x == 0) {
       __stcg(p.out + s, r);
+      if (p.troots) st_relaxed_gpu_u64(p.troots + p.first_item[p.nseg] + s, (uint64_t(tag) << 32) | __float_as_uint(r));
       if (send) send_value(p, s, r);
     }
   }
@@ -424,6 +483,9 @@ __device__ __noinline__ void peer_timeout(const FinishArgs& p) {
   }
 }
 
+template <class Op>
+__device__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag);
+
 // Called by all F finisher CTAs after their segments are written. The last
 // one to arrive resets the counters and runs reduce_cl stage 2: on one GPU
 // directly over the partition values; sharded, it first stores this rank's
@@ -432,10 +494,32 @@ __device__ __noinline__ void peer_timeout(const FinishArgs& p) {
 // region (acquire) and runs the same pairing tree over all P values in
 // partition order — the collective fused into the reduction kernel.
 template <class Op>
-__device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
+__device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag = 0) {
   __shared__ bool last;
   const int tid = threadIdx.x;
   __syncthreads();
+  if (p.troots) {
+    // tagged tail: the last finisher runs stage 2 (its partition values are
+    // read through their tags); the counters are reset at the very end,
+    // once every CTA of the grid has taken its exit ticket
+    if (tid == 0) last = atomicAdd(p.done + 1, 1u) == F - 1;
+    __syncthreads();
+    if (!last) return;
+    if (p.result) stage2_values<Op>(p, F, sm, tag);
+    if (tid == 0) {
+      const uint64_t t0 = global_ns();
+      uint32_t spins = 0;
+      while (ld_acquire_gpu(p.done) < p.grid) {
+        __nanosleep(32);
+        if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();  // cooperative: cannot happen
+      }
+      p.done[0] = 0;
+      p.done[1] = 0;
+      p.done[2] = 0;
+      *p.tag_ctr = tag;  // the next launch's tag is tag + 1
+    }
+    return;
+  }
   if (F == 1) {
     // the only finisher wrote every partition value itself: the barrier
     // orders those stores before the reads below, no ticket needed
@@ -459,7 +543,16 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
     __threadfence();
   }
   if (!p.result) return;
-  if (F == 1 && p.world <= 1 && p.warp_mode && p.nseg && p.nseg <= 32) {
+  stage2_values<Op>(p, F, sm, 0);
+}
+
+// reduce_cl stage 2 proper: the pairing tree over all partition values in
+// partition order (after the NVLink exchange when sharded) into *p.result.
+// tag != 0: this rank's values are read through the tagged slots.
+template <class Op>
+__device__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag) {
+  const int tid = threadIdx.x;
+  if (!tag && F == 1 && p.world <= 1 && p.warp_mode && p.nseg && p.nseg <= 32) {
     // stage 2 over <= 32 values from shared memory by warp 0: the padded
     // pairing tree is 5 xor-shuffle levels (lower lane = left operand)
     if (tid < 32) {
@@ -534,7 +627,9 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
     vals = reinterpret_cast<const float*>(p.peers[p.rank]) + buf;
     nvals = p.p_total;
   }
-  const float root = nvals ? cta_tree<Op>(vals, nvals, sm) : Op::empty();
+  // one GPU, tagged tail: this launch's partition values through their tags
+  const uint64_t* tv = tag && p.world <= 1 ? p.troots + p.first_item[p.nseg] : nullptr;
+  const float root = nvals ? cta_tree<Op>(vals, nvals, sm, tv, tag) : Op::empty();
   if (tid == 0) {
     *p.result = root;
     if (p.world > 1) *p.epoch = epoch;
@@ -577,6 +672,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
+  // tagged tail: this launch's tag (the table's launch counter only moves
+  // at the end of a launch, after every CTA has read it)
+  const uint32_t tag = p.fin.troots ? *reinterpret_cast<volatile uint32_t*>(p.fin.tag_ctr) + 1 : 0;
   // A claim covers kPer consecutive items: one for the read+write map stream,
   // two for the read-only reduction, whose items finish twice as fast and
   // would otherwise saturate the single claim counter.
@@ -613,7 +711,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
       const int64_t valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
       const float r =
           work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
-      if (lane == 0) p.partial[item] = r;
+      if (lane == 0) {
+        if (p.fin.troots) st_relaxed_gpu_u64(p.fin.troots + item, (uint64_t(tag) << 32) | __float_as_uint(r));
+        else p.partial[item] = r;
+      }
     }
     unit = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : unit + nwarps;
   }
@@ -624,10 +725,19 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   const uint32_t F = p.fin.finishers ? p.fin.finishers : uint32_t(umin(G, p.fin.nseg ? p.fin.nseg : 1));
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (!p.fin.troots) __threadfence();  // tagged roots need no fence
     ticket = atomicAdd(p.fin.done, 1u);
   }
   __syncthreads();
+  if (p.fin.troots) {
+    // the FIRST F CTAs out of the stream are the finishers: a partition's
+    // tree starts as soon as its roots carry this launch's tag, while the
+    // grid's last items are still streaming
+    if (ticket >= F) return;
+    segment_values<Op>(p.fin, ticket, F, sm, tag);
+    stage2<Op>(p.fin, F, sm, tag);
+    return;
+  }
   if (ticket + F < G) return;
   if (threadIdx.x == 0) {
     // every CTA is resident (cooperative launch), so the others finish their
@@ -906,7 +1016,9 @@ cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, args);
+  Pass1Args a = args;
+  a.fin.grid = grid;  // the tagged tail's reset waits for every CTA's exit ticket
+  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, a);
 }
 
 template <class Op, bool kMap>
@@ -989,6 +1101,17 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
       f.warp_mode = 1;
       f.finishers = 1;
     }
+  }
+  // tagged tail: cooperative multi-finisher launches with one CTA per
+  // partition tree (UCG_TAGGED_TAIL=0 restores the ticketed tail for A/B)
+  static const bool tagged_ok = [] {
+    const char* e = getenv("UCG_TAGGED_TAIL");
+    return !e || atoi(e) != 0;
+  }();
+  if (tagged_ok && fused_finish && !f.warp_mode && f.finishers != 1 && !f.ntaper && !f.flag_exchange && t->d_troots &&
+      dynamic_items() && !getenv("UCG_PDL_MULTI")) {
+    f.troots = t->d_troots;
+    f.tag_ctr = t->d_done + 3;
   }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
