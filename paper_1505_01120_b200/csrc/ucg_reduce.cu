@@ -216,8 +216,10 @@ __device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// (no "memory" clobber: the tag validates the slot on its own, so the store
+// needs no ordering against the stream's other loads and stores)
 __device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 
 // Tagged values (the tagged tail): slot = {tag << 32 | float bits}, written
@@ -239,23 +241,28 @@ __device__ __forceinline__ void load_tagged16(const uint64_t* slots, uint64_t ba
 #pragma unroll
     for (int k = 0; k < kTreeVals; ++k) q[k] = base + k < n ? ld_relaxed_gpu_u64(slots + base + k) : 0;
   }
+  // every pending slot is re-read in the same round (all loads in flight at
+  // once), one short sleep per round: the wait ends within one round of the
+  // last slot's store instead of accumulating a back-off per slot
+  uint32_t pending = 0;
 #pragma unroll
-  for (int k = 0; k < kTreeVals; ++k) {
-    if (base + k >= n) {
-      v[k] = ident;
-      continue;
+  for (int k = 0; k < kTreeVals; ++k)
+    if (base + k < n && uint32_t(q[k] >> 32) != tag) pending |= 1u << k;
+  if (pending) {
+    const uint64_t t0 = global_ns();
+    while (pending) {
+      __nanosleep(128);
+#pragma unroll
+      for (int k = 0; k < kTreeVals; ++k)
+        if ((pending >> k) & 1) q[k] = ld_relaxed_gpu_u64(slots + base + k);
+#pragma unroll
+      for (int k = 0; k < kTreeVals; ++k)
+        if (((pending >> k) & 1) && uint32_t(q[k] >> 32) == tag) pending &= ~(1u << k);
+      if (pending && global_ns() - t0 > kPeerWaitNs) __trap();  // a writer of this launch never stored: cannot happen
     }
-    if (uint32_t(q[k] >> 32) != tag) {
-      const uint64_t t0 = global_ns();
-      uint32_t ns = 64;
-      while (uint32_t((q[k] = ld_relaxed_gpu_u64(slots + base + k)) >> 32) != tag) {
-        __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : ns;
-        if (global_ns() - t0 > kPeerWaitNs) __trap();  // a writer of this launch never stored: cannot happen
-      }
-    }
-    v[k] = __uint_as_float(uint32_t(q[k]));
   }
+#pragma unroll
+  for (int k = 0; k < kTreeVals; ++k) v[k] = base + k < n ? __uint_as_float(uint32_t(q[k])) : ident;
 }
 
 template <class Op>
@@ -352,6 +359,7 @@ struct FinishArgs {
   uint64_t* troots;           // [nitems] item slots, then [nseg] partition-value slots
   uint32_t* tag_ctr;          // launches completed on this table (this launch's tag = *tag_ctr + 1)
   uint32_t grid;              // CTAs of the launch (the tagged tail's reset waits for all tickets)
+  int tagged_last;            // A/B: tagged slots, but the last F CTAs out finish (after the grid)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -732,9 +740,19 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   if (p.fin.troots) {
     // the FIRST F CTAs out of the stream are the finishers: a partition's
     // tree starts as soon as its roots carry this launch's tag, while the
-    // grid's last items are still streaming
-    if (ticket >= F) return;
-    segment_values<Op>(p.fin, ticket, F, sm, tag);
+    // grid's last items are still streaming (tagged_last, A/B: the last F
+    // CTAs out, after the whole grid, as the ticketed tail but without fences)
+    uint32_t j = ticket;
+    if (p.fin.tagged_last) {
+      if (ticket + F < G) return;
+      j = ticket + F - G;
+      if (threadIdx.x == 0)
+        while (ld_acquire_gpu(p.fin.done) < G) __nanosleep(32);
+      __syncthreads();
+    } else if (ticket >= F) {
+      return;
+    }
+    segment_values<Op>(p.fin, j, F, sm, tag);
     stage2<Op>(p.fin, F, sm, tag);
     return;
   }
@@ -1112,6 +1130,8 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
       dynamic_items() && !getenv("UCG_PDL_MULTI")) {
     f.troots = t->d_troots;
     f.tag_ctr = t->d_done + 3;
+    static const bool tagged_last = getenv("UCG_TAGGED_LAST") != nullptr;
+    f.tagged_last = tagged_last ? 1 : 0;
   }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
