@@ -160,8 +160,9 @@ inline DeviceOp affine_f32(float a, float b) {
     const auto off = detail::pack_offsets(sizes, packed ? 1 : 64, &total);
     float* x = static_cast<float*>(g.scratch(0).ensure(total * 4));
     float* y = static_cast<float*>(g.scratch(1).ensure(total * 4));
-    HostPipe& pipe = g.attached<HostPipe>();
     std::vector<std::vector<float>> outs(in.size());
+    HostPipe& pipe = g.attached<HostPipe>();
+    HostPipe::Scope pipe_scope(pipe);  // drains before outs / in / off go, also when a call throws
     if (packed) {
       // many small elements: packed into slots, one launch, packed back
       pipe.upload_pieces(x, detail::as_bytes(in), detail::scaled(off, 4));
@@ -213,6 +214,7 @@ inline DeviceOp partition_reduce_f32(kernels::ReduceOp rop) {
     const auto off = detail::pack_offsets(sizes, 64, &total);
     float* x = static_cast<float*>(g.scratch(0).ensure(total * 4));
     HostPipe& pipe = g.attached<HostPipe>();
+    HostPipe::Scope pipe_scope(pipe);
     pipe.upload_pieces(x, detail::as_bytes(in), detail::scaled(off, 4));
     pipe.compute_after_upload();
     ucg_segtab* tab = nullptr;
@@ -281,13 +283,14 @@ std::vector<ucores::Element> elementwise_tasks(Gpu& g, TaskBatch tasks, int code
   T* a = static_cast<T*>(g.scratch(0).ensure(total * sizeof(T)));
   T* b = static_cast<T*>(g.scratch(1).ensure(total * sizeof(T)));
   T* c = static_cast<T*>(g.scratch(2).ensure(total * sizeof(T)));
+  std::vector<std::vector<T>> outs;
   HostPipe& pipe = g.attached<HostPipe>();
+  HostPipe::Scope pipe_scope(pipe);
   pipe.upload_pieces(a, detail::as_bytes(A), detail::scaled(off, sizeof(T)));
   pipe.upload_pieces(b, detail::as_bytes(B), detail::scaled(off, sizeof(T)));
   pipe.compute_after_upload();
   if constexpr (std::is_same_v<T, float>) check(ucg_elementwise2_f32(a, b, c, total, code, g.stream()));
   else check(ucg_elementwise2_i64(a, b, c, total, g.stream()));
-  std::vector<std::vector<T>> outs;
   pipe.download_pieces(&outs, c, sizes, off);
   pipe.drain();
   return detail::to_elements(std::move(outs));
@@ -385,12 +388,13 @@ inline DeviceOp sobel(std::size_t width) {
     const auto out_off = detail::pack_offsets(out_sz, 16, &tout);
     std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(tin));
     std::uint8_t* dout = static_cast<std::uint8_t*>(g.scratch(1).ensure(tout));
+    std::vector<std::vector<std::uint8_t>> outs;
     HostPipe& pipe = g.attached<HostPipe>();
+    HostPipe::Scope pipe_scope(pipe);
     pipe.upload_pieces(din, in, in_off);
     pipe.compute_after_upload();
     check(ucg_sobel_bands_u8(din, in_off.data(), dout, out_off.data(), rows.data(), rows.size(), width,
                              g.stream()));
-    std::vector<std::vector<std::uint8_t>> outs;
     pipe.download_pieces(&outs, dout, out_sz, out_off);
     pipe.drain();
     return detail::to_elements(std::move(outs));
@@ -427,14 +431,15 @@ inline DeviceOp wordcount(std::uint64_t min_device_bytes) {
     const auto off = detail::pack_offsets(sizes, 16, &total);
     std::uint8_t* din = static_cast<std::uint8_t*>(g.scratch(0).ensure(total));
     std::uint8_t* dfl = static_cast<std::uint8_t*>(g.scratch(1).ensure(total));
+    std::vector<std::uint8_t> flags;
     HostPipe& pipe = g.attached<HostPipe>();
+    HostPipe::Scope pipe_scope(pipe);
     pipe.upload_pieces(din, in, off);
     pipe.compute_after_upload();
     for (std::size_t i = 0; i < in.size(); ++i) {
       if (sizes[i] < min_device_bytes || !sizes[i]) continue;
       check(ucg_word_start_flags(din + off[i], sizes[i], dfl + off[i], g.stream()));
     }
-    std::vector<std::uint8_t> flags;
     pipe.download(&flags, dfl, total);
     pipe.drain();
     std::vector<ucores::Element> out;
@@ -481,6 +486,7 @@ inline DeviceOp matmul_tc(std::size_t n, bool fp32_faithful = true) {
     // two device slots: task i+1's upload overlaps task i's product, task
     // i's C download overlaps task i+1's
     HostPipe& pipe = g.attached<HostPipe>();
+    HostPipe::Scope pipe_scope(pipe);
     for (std::size_t i = 0; i < tasks.size(); ++i) {
       float* dab = static_cast<float*>(g.scratch(4 + 2 * (i & 1)).ensure(2 * n * n * 4));
       float* dc = static_cast<float*>(g.scratch(5 + 2 * (i & 1)).ensure(n * n * 4));

@@ -225,6 +225,27 @@ class HostPipe {
 
   Gpu& gpu() { return *gpu_; }
 
+  /// Drains the pipe on scope exit, stack unwinding included: declare it
+  /// after the vectors the pipe's pending copy tasks read or write, so a
+  /// call that throws mid-wave never leaves a pool thread writing into a
+  /// destroyed vector. Errors already reported by the throwing call are
+  /// not raised again.
+  class Scope {
+   public:
+    explicit Scope(HostPipe& p) : p_(p) {}
+    Scope(const Scope&) = delete;
+    Scope& operator=(const Scope&) = delete;
+    ~Scope() {
+      try {
+        p_.drain();
+      } catch (...) {
+      }
+    }
+
+   private:
+    HostPipe& p_;
+  };
+
   /// Host bytes -> device, through the in ring (parallel copy-in, DMA on the
   /// copy-in stream). The compute stream is NOT yet ordered after it: call
   /// compute_after_upload() before launching on the data.
