@@ -335,11 +335,11 @@ class HostPipe {
       for (int k = 0; k < parts; ++k) {
         const std::uint64_t b = m * k / parts, e = m * (k + 1) / parts;
         pending_.push_back(work_pool().submit([dst, off, b, e, &s, ready] {
+          Release rel(s);  // the slot is released even if this task fails
           ready->wait();
           check(ucg_event_synchronize(s.ev));
           std::memcpy(reinterpret_cast<std::uint8_t*>(dst->data()) + off + b,
                       static_cast<const std::uint8_t*>(s.buf) + b, e - b);
-          s.drains.fetch_sub(1);
         }));
       }
     }
@@ -372,6 +372,7 @@ class HostPipe {
       const std::size_t k0 = i, k1 = j;
       // one vector per piece: the allocations are spread over the pool
       pending_.push_back(work_pool().submit([&s, dst, &sizes, &off, k0, k1, base] {
+        Release rel(s);
         check(ucg_event_synchronize(s.ev));
         const T* h = static_cast<const T*>(s.buf);
         constexpr std::size_t kBlk = 2048;
@@ -380,7 +381,6 @@ class HostPipe {
           for (std::size_t k = k0 + blk * kBlk; k < e; ++k)
             (*dst)[k].assign(h + off[k] - base, h + off[k] - base + sizes[k]);
         });
-        s.drains.fetch_sub(1);
       }));
       i = j;
     }
@@ -418,6 +418,12 @@ class HostPipe {
   struct Ring {
     Slot slot[kSlots];
     int next = 0;
+  };
+  // releases one drain task's hold on an out slot when the task ends
+  struct Release {
+    Slot& s;
+    explicit Release(Slot& slot) : s(slot) {}
+    ~Release() { s.drains.fetch_sub(1); }
   };
 
   Slot& acquire_in() {
