@@ -1234,11 +1234,14 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.tag_ctr = t->d_done + 3;
     static const bool tagged_last = getenv("UCG_TAGGED_LAST") != nullptr;
     f.tagged_last = tagged_last ? 1 : 0;
-    // chunk tail of the fused map (UCG_CHUNK_TAIL=0: off, for A/B); needs
-    // at least 2 chunks of the variant's 128*U floats per item
+    // chunk tail of the fused map (A/B, off by default: UCG_CHUNK_TAIL=1;
+    // measured neutral to slower — 8-partition shard 169.96-170.7 vs 169.65
+    // us, 2^30 1275-1280 vs 1274 us — the claim counter takes the extra
+    // claims at the end, and the tail is not item-length bound); needs at
+    // least 2 chunks of the variant's 128*U floats per item
     static const bool chunk_tail_on = [] {
       const char* e = getenv("UCG_CHUNK_TAIL");
-      return !e || atoi(e) != 0;
+      return e && atoi(e) != 0;
     }();
     const int u = kPass1Variants[pass1_variant()].u;
     if (chunk_tail_on && y && t->ctail_items && t->d_csub && (uint64_t(1) << t->item_log2) >= 2ull * 128 * u) {
