@@ -243,6 +243,51 @@ class DeviceEngine {
     return out;
   }
 
+  /// Ingestion without host Elements: the device twin of
+  /// ucores::create_dataset (dataset.hpp:64-82) over caller-owned host
+  /// arrays — element i is `elements[i]` (kind `kind`, bytes), distributed
+  /// over `num_partitions` contiguous partitions ceiling-first, and copied
+  /// straight from the caller's memory through each GPU's transfer
+  /// pipeline. Errors as create_dataset: InvalidPartitionCount for 0
+  /// partitions. The caller's arrays may be reused once this returns.
+  DeviceDataset create_dataset(const std::vector<std::span<const std::uint8_t>>& elements, ucores::ElementKind kind,
+                               std::size_t num_partitions) {
+    if (num_partitions < 1)
+      throw ucores::InvalidPartitionCount("num_partitions must be >= 1, got " + std::to_string(num_partitions));
+    const std::size_t eb = entry_bytes(kind), n = elements.size();
+    const std::size_t base = n / num_partitions, extra = n % num_partitions;
+    std::vector<DevicePartition> parts(num_partitions);
+    std::vector<std::size_t> first(num_partitions + 1, 0);
+    for (std::size_t p = 0; p < num_partitions; ++p) {
+      const std::size_t take = base + (p < extra ? 1 : 0);
+      first[p + 1] = first[p] + take;
+      parts[p].gpu = gpu_of(p, num_partitions);
+      parts[p].kind = take ? kind : ucores::ElementKind::ByteArray;  // an empty partition concatenates to bytes
+      for (std::size_t i = first[p]; i < first[p + 1]; ++i) {
+        if (elements[i].size() % eb)
+          throw ucores::ElementKindError("element " + std::to_string(i) + " is not a whole number of entries");
+        parts[p].sizes.push_back(elements[i].size() / eb);
+      }
+    }
+    DeviceDataset out = allocate(std::move(parts));
+    run_per_gpu([&](std::size_t g) {
+      HostPipe& pipe = gpus_[g]->attached<HostPipe>();
+      for (std::size_t p = 0; p < num_partitions; ++p) {
+        if (out.parts_[p].gpu != g) continue;
+        std::vector<std::span<const std::uint8_t>> pieces(elements.begin() + first[p], elements.begin() + first[p + 1]);
+        std::vector<std::uint64_t> off;
+        std::uint64_t at = 0;
+        for (const auto& e : pieces) {
+          off.push_back(at);
+          at += e.size();
+        }
+        pipe.upload_pieces(out.data(p), pieces, off);
+      }
+      pipe.compute_after_upload();
+    });
+    return out;
+  }
+
   /// HBM -> host Dataset (the lazy collect of SURVEY §8(f)1).
   ucores::Dataset collect(const DeviceDataset& d) {
     std::vector<ucores::Partition> parts(d.partition_count());

@@ -375,6 +375,40 @@ int main() {
     EXPECT(same(d, de.collect(de.upload(d))), "collect(upload(d)) == d");
   });
 
+  run_case("device dataset: create_dataset from host arrays == upload(ucores::create_dataset)", [&] {
+    for (auto [count, parts, len] : std::vector<std::tuple<std::size_t, std::size_t, std::size_t>>{
+             {10, 3, 5}, {7, 9, 1000}, {64, 8, 1u << 16}, {1u << 12, 4, 1}}) {
+      std::vector<std::vector<float>> es(count, std::vector<float>(len));
+      for (std::size_t i = 0; i < count; ++i)
+        for (std::size_t j = 0; j < len; ++j) es[i][j] = u01(31 + i, j);
+      std::vector<std::span<const std::uint8_t>> spans;
+      std::vector<Element> host;
+      for (const auto& v : es) {
+        spans.emplace_back(reinterpret_cast<const std::uint8_t*>(v.data()), v.size() * 4);
+        host.push_back(Element::f32(v));
+      }
+      Dataset hd = create_dataset(std::move(host), parts);
+      DeviceDataset dd = de.create_dataset(spans, ElementKind::F32Array, parts);
+      EXPECT(same(hd, de.collect(dd)), "create_dataset partitions and payloads");
+      for (const char* op : {"sum", "max"}) {
+        const std::string pk = std::string("p") + op, rk = std::string(op) + "2";
+        bool empty = false;
+        for (const Partition& p : hd.partitions()) empty |= p.elements.empty();
+        if (empty) continue;  // map_cl_partition over an empty partition fails in both engines
+        EXPECT(eh.reduce_cl(eh.map_cl_partition(eh.map_cl(hd, "axpb"), pk), rk) ==
+                   de.reduce_cl(de.map_cl_partition(de.map_cl(dd, "axpb"), pk), rk),
+               "chain over the ingested dataset");
+      }
+    }
+    bool threw = false;
+    try {
+      de.create_dataset({}, ElementKind::F32Array, 0);
+    } catch (const InvalidPartitionCount&) {
+      threw = true;
+    }
+    EXPECT(threw, "0 partitions -> InvalidPartitionCount");
+  });
+
   run_case("device dataset: C1 chains bitwise vs host Engine (packed and ragged elements)", [&] {
     for (auto [n, elems, parts] : std::vector<std::tuple<std::size_t, std::size_t, std::size_t>>{
              {1u << 20, 4, 4}, {100003, 13, 5}, {70001, 7, 3}, {4099, 33, 6}}) {
