@@ -130,9 +130,6 @@ struct ucg_segtab {
   uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches),
                            // [3] launches completed (the tagged tail's tag source)
   uint64_t* d_troots;      // [nitems + nseg] {tag, value} slots of the tagged tail (zeroed at creation)
-  uint64_t ctail_items;    // chunk tail: the last ctail_items items are claimed a chunk at a time
-  uint64_t* d_csub;        // [ctail_items * 2^(item_log2 - 8)] {tag, chunk root} slots (zeroed)
-  uint32_t* d_ccnt;        // [ctail_items] chunk counters (zeroed; a launch adds the chunk count)
   uint64_t ntaper;         // trailing items the fused map streams as 4 sub-items each (0: none)
 };
 

@@ -227,7 +227,7 @@ __device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
 // launch's tag has the value — no fence on the writer's side. Each thread
 // loads its 16 slots, then re-polls (with backoff) only the ones whose tag is
 // not this launch's yet.
-__device__ __forceinline__ void load_tagged16(const uint64_t* slots, uint64_t base, uint64_t n, uint32_t tag,
+__device__ __noinline__ void load_tagged16(const uint64_t* slots, uint64_t base, uint64_t n, uint32_t tag,
                                               float (&v)[kTreeVals], float ident) {
   uint64_t q[kTreeVals];
   if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(slots + base) & 15) == 0) {
@@ -360,14 +360,6 @@ struct FinishArgs {
   uint32_t* tag_ctr;          // launches completed on this table (this launch's tag = *tag_ctr + 1)
   uint32_t grid;              // CTAs of the launch (the tagged tail's reset waits for all tickets)
   int tagged_last;            // A/B: tagged slots, but the last F CTAs out finish (after the grid)
-  // chunk tail (fused map with the tagged tail): items [ctail_first, nitems)
-  // are claimed one chunk at a time, so the stream's last wave is a chunk,
-  // not an item, long; csub = {tag, chunk root} slots, ccnt = chunks done
-  // per tail item (cumulative over launches: a launch adds exactly the
-  // item's chunk count, so (old + 1) % chunks == 0 marks the item's last)
-  uint64_t ctail_first;       // == nitems: no chunk tail
-  uint64_t* csub;
-  uint32_t* ccnt;
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -500,7 +492,7 @@ __device__ __noinline__ void peer_timeout(const FinishArgs& p) {
 }
 
 template <class Op>
-__device__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag);
+__device__ __noinline__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag);
 
 // Called by all F finisher CTAs after their segments are written. The last
 // one to arrive resets the counters and runs reduce_cl stage 2: on one GPU
@@ -566,7 +558,7 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t t
 // partition order (after the NVLink exchange when sharded) into *p.result.
 // tag != 0: this rank's values are read through the tagged slots.
 template <class Op>
-__device__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag) {
+__device__ __noinline__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag) {
   const int tid = threadIdx.x;
   if (!tag && F == 1 && p.world <= 1 && p.warp_mode && p.nseg && p.nseg <= 32) {
     // stage 2 over <= 32 values from shared memory by warp 0: the padded
@@ -661,8 +653,6 @@ __device__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uin
 // CTA, no kernel boundary between the stream and the trees. (Finishing
 // segments with a per-item last-warp counter was measured 5% slower: the
 // fence after each item waits for that warp's 32-64 KB of y stores.)
-struct Pass1Args;
-
 struct Pass1Args {
   const float* x;
   float* y;
@@ -678,89 +668,6 @@ struct Pass1Args {
   int dynamic;  // claim items from the counter fin.done[2] instead of grid-stride
   FinishArgs fin;
 };
-
-// The fused map's last items, one chunk per claim (see FinishArgs): the
-// claim for the unit after next is issued, and the next unit's loads are in
-// flight, while the current chunk is mapped, stored and reduced — the same
-// one-chunk-ahead pipeline as inside an item, now across claims. A chunk's
-// root goes to its tagged slot; the warp whose chunk completes an item (the
-// item's counter) combines the item's chunk roots in the tree order
-// work_item uses (balanced over the chunks, lower index left) and writes the
-// item's tagged root, which the finishers read as for any other item.
-template <class Op, int U>
-__device__ void chunk_tail(const Pass1Args& p, uint64_t u, uint64_t nwarps, uint32_t tag, int lane) {
-  constexpr int kChunk = 128 * U;
-  const uint32_t cpi = uint32_t((uint64_t(1) << p.item_log2) / kChunk);
-  const uint64_t nfull = p.fin.ctail_first;
-  const uint64_t end = nfull + (p.nitems - nfull) * cpi;
-  auto decode = [&](uint64_t unit, uint64_t& item, uint32_t& c, uint64_t& off, int64_t& valid) {
-    const uint64_t cu = unit - nfull;
-    item = nfull + cu / cpi;
-    c = uint32_t(cu % cpi);
-    const uint32_t sg = p.item_seg[item];
-    const uint64_t start = ((item - p.first_item[sg]) << p.item_log2) + uint64_t(c) * kChunk;
-    off = p.begin[sg] + start;
-    valid = int64_t(p.len[sg]) - int64_t(start);  // <= 0: an empty chunk of a segment's last item
-  };
-  auto load = [&](uint64_t off, int64_t valid, float4 (&v)[U]) {
-    if (valid >= kChunk) chunk_load<Op, false, U>(p.x + off, kChunk, lane, v);
-    else if (valid > 0) chunk_load<Op, true, U>(p.x + off, valid, lane, v);
-  };
-  uint32_t claim = 0;
-  if (lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
-  uint64_t item, off;
-  uint32_t c;
-  int64_t valid;
-  decode(u, item, c, off, valid);
-  float4 cur[U];
-  load(off, valid, cur);
-#pragma unroll 1
-  for (;;) {
-    const uint64_t next = nwarps + __shfl_sync(kFull, claim, 0);
-    const bool more = next < end;
-    uint64_t nitem = 0, noff = 0;
-    uint32_t nc = 0;
-    int64_t nvalid = 0;
-    float4 nxt[U];
-    if (more) {
-      if (lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
-      decode(next, nitem, nc, noff, nvalid);
-      load(noff, nvalid, nxt);
-    }
-    float r = Op::identity();
-    if (valid >= kChunk) r = chunk_finish<Op, true, false, U>(cur, p.y + off, kChunk, p.a, p.b, lane);
-    else if (valid > 0) r = chunk_finish<Op, true, true, U>(cur, p.y + off, valid, p.a, p.b, lane);
-    const uint64_t ti = item - nfull;
-    uint32_t last = 0;
-    if (lane == 0) {
-      st_relaxed_gpu_u64(p.fin.csub + ti * cpi + c, (uint64_t(tag) << 32) | __float_as_uint(r));
-      last = (atomicAdd(p.fin.ccnt + ti, 1u) + 1) % cpi == 0;
-    }
-    if (__shfl_sync(kFull, last, 0)) {
-      float v = Op::identity();
-      if (uint32_t(lane) < cpi) {
-        const uint64_t* slot = p.fin.csub + ti * cpi + lane;
-        uint64_t q;
-        const uint64_t t0 = global_ns();
-        while (uint32_t((q = ld_relaxed_gpu_u64(slot)) >> 32) != tag) {
-          __nanosleep(64);
-          if (global_ns() - t0 > kPeerWaitNs) __trap();  // a chunk of this launch never stored: cannot happen
-        }
-        v = __uint_as_float(uint32_t(q));
-      }
-#pragma unroll 1
-      for (uint32_t j = 1; j < cpi; j <<= 1) v = lr<Op>(v, __shfl_xor_sync(kFull, v, j), !(lane & j));
-      if (lane == 0) st_relaxed_gpu_u64(p.fin.troots + item, (uint64_t(tag) << 32) | __float_as_uint(v));
-    }
-    if (!more) return;
-#pragma unroll
-    for (int k = 0; k < U; ++k) cur[k] = nxt[k];
-    item = nitem;
-    c = nc;
-    off = noff;
-    valid = nvalid;
-  }
-}
 
 template <class Op, bool kMap, int U, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const __grid_constant__ Pass1Args p) {
@@ -784,17 +691,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   // quarter of an item each, so the last warps finish close together.
   const uint64_t ntaper = kMap ? p.fin.ntaper : 0;
   const uint64_t units_end = ntaper ? p.fin.taper_first + 4 * ntaper : 0;
-  // chunk tail (fused map, tagged tail, claimed items): units from
-  // ctail_first on are chunks of the last items
-  const bool ctail = kMap && p.fin.csub != nullptr;
-  const uint64_t nfull = ctail ? p.fin.ctail_first : p.nitems;
   uint64_t unit = warp;
-  while (ntaper ? unit < units_end : unit * kPer < p.nitems || (ctail && unit >= nfull)) {
-    if (ctail && unit >= nfull) {
-      if (unit < nfull + (p.nitems - nfull) * ((uint64_t(1) << p.item_log2) / (128 * U)))
-        chunk_tail<Op, U>(p, unit, nwarps, tag, lane);
-      break;
-    }
+  while (ntaper ? unit < units_end : unit * kPer < p.nitems) {
     // dynamic: the next unit is claimed now and consumed after this one
     uint32_t claim = 0;
     if (p.dynamic && lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
@@ -839,40 +737,30 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
     ticket = atomicAdd(p.fin.done, 1u);
   }
   __syncthreads();
-  if (p.fin.troots) {
-    // the FIRST F CTAs out of the stream are the finishers: a partition's
-    // tree starts as soon as its roots carry this launch's tag, while the
-    // grid's last items are still streaming (tagged_last, A/B: the last F
-    // CTAs out, after the whole grid, as the ticketed tail but without fences)
-    uint32_t j = ticket;
-    if (p.fin.tagged_last) {
-      if (ticket + F < G) return;
-      j = ticket + F - G;
-      if (threadIdx.x == 0)
-        while (ld_acquire_gpu(p.fin.done) < G) __nanosleep(32);
-      __syncthreads();
-    } else if (ticket >= F) {
-      return;
+  // tagged tail: the FIRST F CTAs out of the stream are the finishers — a
+  // partition's tree starts as soon as its roots carry this launch's tag,
+  // while the grid's last items are still streaming. Ticketed tail (and the
+  // tagged_last A/B): the LAST F CTAs out, once the whole grid has left the
+  // stream. One call site for the partition trees and stage 2 (the kernel's
+  // code size shows in the latency-bound C1 step).
+  const bool early = p.fin.troots && !p.fin.tagged_last;
+  if (early ? ticket >= F : ticket + F < G) return;
+  if (!early) {
+    if (threadIdx.x == 0) {
+      // every CTA is resident (cooperative launch), so the others finish their
+      // stream; a wait of kPeerWaitNs cannot happen — trap rather than reduce
+      // item roots that are not all written
+      const uint64_t t0 = global_ns();
+      uint32_t spins = 0;
+      while (ld_acquire_gpu(p.fin.done) < G) {
+        __nanosleep(32);
+        if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();
+      }
     }
-    segment_values<Op>(p.fin, j, F, sm, tag);
-    stage2<Op>(p.fin, F, sm, tag);
-    return;
+    __syncthreads();
   }
-  if (ticket + F < G) return;
-  if (threadIdx.x == 0) {
-    // every CTA is resident (cooperative launch), so the others finish their
-    // stream; a wait of kPeerWaitNs cannot happen — trap rather than reduce
-    // item roots that are not all written
-    const uint64_t t0 = global_ns();
-    uint32_t spins = 0;
-    while (ld_acquire_gpu(p.fin.done) < G) {
-      __nanosleep(32);
-      if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();
-    }
-  }
-  __syncthreads();
-  segment_values<Op>(p.fin, ticket + F - G, F, sm);
-  stage2<Op>(p.fin, F, sm);
+  segment_values<Op>(p.fin, early ? ticket : ticket + F - G, F, sm, tag);
+  stage2<Op>(p.fin, F, sm, tag);
 }
 
 // Stand-alone finish (tables with no work items, or UCG_SEPARATE_FINISH=1):
@@ -1234,21 +1122,6 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.tag_ctr = t->d_done + 3;
     static const bool tagged_last = getenv("UCG_TAGGED_LAST") != nullptr;
     f.tagged_last = tagged_last ? 1 : 0;
-    // chunk tail of the fused map (A/B, off by default: UCG_CHUNK_TAIL=1;
-    // measured neutral to slower — 8-partition shard 169.96-170.7 vs 169.65
-    // us, 2^30 1275-1280 vs 1274 us — the claim counter takes the extra
-    // claims at the end, and the tail is not item-length bound); needs at
-    // least 2 chunks of the variant's 128*U floats per item
-    static const bool chunk_tail_on = [] {
-      const char* e = getenv("UCG_CHUNK_TAIL");
-      return e && atoi(e) != 0;
-    }();
-    const int u = kPass1Variants[pass1_variant()].u;
-    if (chunk_tail_on && y && t->ctail_items && t->d_csub && (uint64_t(1) << t->item_log2) >= 2ull * 128 * u) {
-      f.ctail_first = t->nitems - t->ctail_items;
-      f.csub = t->d_csub;
-      f.ccnt = t->d_ccnt;
-    }
   }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,

@@ -359,8 +359,6 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
     cudaFree(t->d_item_seg);
     cudaFree(t->d_done);
     cudaFree(t->d_troots);
-    cudaFree(t->d_csub);
-    cudaFree(t->d_ccnt);
     delete t;
     return cuda_fail(e, what);
   };
@@ -374,17 +372,7 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   // tagged-tail slots, zero = no launch's tag (tags start at 1)
   if ((e = cudaMalloc(&t->d_troots, (nitems + nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMemset(t->d_troots, 0, (nitems + nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMemset");
-  // chunk tail: about one wave of the fused map's warps (2 CTAs x 8 warps
-  // per SM) of items, at most half of the table
-  t->ctail_items = std::min<uint64_t>(nitems / 2, uint64_t(sm_count()) * 16);
-  if (const char* ce = getenv("UCG_CTAIL_ITEMS")) t->ctail_items = std::min<uint64_t>(nitems / 2, uint64_t(atoll(ce)));  // A/B
-  if (t->ctail_items) {
-    const uint64_t nsub = t->ctail_items << (item_log2 - 8);  // enough chunk slots for the smallest chunk (256 floats)
-    if ((e = cudaMalloc(&t->d_csub, nsub * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-    if ((e = cudaMemset(t->d_csub, 0, nsub * 8)) != cudaSuccess) return cleanup(e, "cudaMemset");
-    if ((e = cudaMalloc(&t->d_ccnt, t->ctail_items * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-    if ((e = cudaMemset(t->d_ccnt, 0, t->ctail_items * 4)) != cudaSuccess) return cleanup(e, "cudaMemset");
-  }
+
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
@@ -407,8 +395,6 @@ int ucg_segtab_destroy(ucg_segtab* t) {
   cudaFree(t->d_item_seg);
   cudaFree(t->d_done);
   cudaFree(t->d_troots);
-  cudaFree(t->d_csub);
-  cudaFree(t->d_ccnt);
   if (cur >= 0 && cur != t->device) cudaSetDevice(cur);
   delete t;
   return UCG_OK;
