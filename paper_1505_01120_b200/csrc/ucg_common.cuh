@@ -127,9 +127,7 @@ struct ucg_segtab {
   uint32_t* d_item_seg;    // [nitems]
   uint64_t max_items_per_seg;
   int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
-  uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches),
-                           // [3] launches completed (the tagged tail's tag source)
-  uint64_t* d_troots;      // [nitems + nseg] {tag, value} slots of the tagged tail (zeroed at creation)
+  uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches)
   uint64_t ntaper;         // trailing items the fused map streams as 4 sub-items each (0: none)
 };
 

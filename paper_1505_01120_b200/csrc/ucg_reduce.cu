@@ -211,71 +211,14 @@ struct TreeSmem {
 // shuffles (lower lane = left operand), thread 0 the last 3 over the warp
 // roots — one barrier per block. Block roots are merged by a binary-counter
 // stack of aligned subtrees and the stack is folded right to left.
-__device__ __forceinline__ uint64_t ld_relaxed_gpu_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-// (no "memory" clobber: the tag validates the slot on its own, so the store
-// needs no ordering against the stream's other loads and stores)
-__device__ __forceinline__ void st_relaxed_gpu_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v));
-}
-
-// Tagged values (the tagged tail): slot = {tag << 32 | float bits}, written
-// with ONE 64-bit store (single-copy atomic), so a reader that sees this
-// launch's tag has the value — no fence on the writer's side. Each thread
-// loads its 16 slots, then re-polls (with backoff) only the ones whose tag is
-// not this launch's yet.
-__device__ __noinline__ void load_tagged16(const uint64_t* slots, uint64_t base, uint64_t n, uint32_t tag,
-                                              float (&v)[kTreeVals], float ident) {
-  uint64_t q[kTreeVals];
-  if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(slots + base) & 15) == 0) {
-#pragma unroll
-    for (int k = 0; k < kTreeVals / 2; ++k)
-      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
-                   : "=l"(q[2 * k]), "=l"(q[2 * k + 1])
-                   : "l"(slots + base + 2 * k)
-                   : "memory");
-  } else {
-#pragma unroll
-    for (int k = 0; k < kTreeVals; ++k) q[k] = base + k < n ? ld_relaxed_gpu_u64(slots + base + k) : 0;
-  }
-  // every pending slot is re-read in the same round (all loads in flight at
-  // once), one short sleep per round: the wait ends within one round of the
-  // last slot's store instead of accumulating a back-off per slot
-  uint32_t pending = 0;
-#pragma unroll
-  for (int k = 0; k < kTreeVals; ++k)
-    if (base + k < n && uint32_t(q[k] >> 32) != tag) pending |= 1u << k;
-  if (pending) {
-    const uint64_t t0 = global_ns();
-    while (pending) {
-      __nanosleep(128);
-#pragma unroll
-      for (int k = 0; k < kTreeVals; ++k)
-        if ((pending >> k) & 1) q[k] = ld_relaxed_gpu_u64(slots + base + k);
-#pragma unroll
-      for (int k = 0; k < kTreeVals; ++k)
-        if (((pending >> k) & 1) && uint32_t(q[k] >> 32) == tag) pending &= ~(1u << k);
-      if (pending && global_ns() - t0 > kPeerWaitNs) __trap();  // a writer of this launch never stored: cannot happen
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < kTreeVals; ++k) v[k] = base + k < n ? __uint_as_float(uint32_t(q[k])) : ident;
-}
-
 template <class Op>
-__device__ float cta_tree(const float* __restrict__ vals, uint64_t n, TreeSmem& sm,
-                          const uint64_t* tagged = nullptr, uint32_t tag = 0) {
+__device__ float cta_tree(const float* __restrict__ vals, uint64_t n, TreeSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint64_t nblocks = (n + kTreeBlock - 1) / kTreeBlock;
   for (uint64_t bi = 0; bi < nblocks; ++bi) {
     const uint64_t base = bi * kTreeBlock + kTreeVals * uint64_t(tid);
     float v[kTreeVals];
-    if (tagged) {
-      load_tagged16(tagged, base, n, tag, v, Op::identity());
-    } else if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(vals + base) & 15) == 0) {
+    if (base + kTreeVals <= n && (reinterpret_cast<uintptr_t>(vals + base) & 15) == 0) {
       // 4 x 16-byte loads (a quarter of the L2 sector requests of scalar loads)
 #pragma unroll
       for (int k = 0; k < kTreeVals / 4; ++k) {
@@ -351,15 +294,6 @@ struct FinishArgs {
                               // values as it computes them (stage 2 only receives)
   float* sub;                 // tapered tail: 4 sub-item roots per item in [taper_first, +ntaper)
   uint64_t taper_first, ntaper;
-  // tagged tail (cooperative multi-finisher CTA-mode launches): item roots
-  // and partition values as {tag, value} slots of the segment table, so the
-  // FIRST F CTAs out of the stream start the partition trees while the last
-  // items are still streaming, with no fence per CTA and no wait for the
-  // grid; null: the ticketed tail (last F CTAs out, after the whole grid)
-  uint64_t* troots;           // [nitems] item slots, then [nseg] partition-value slots
-  uint32_t* tag_ctr;          // launches completed on this table (this launch's tag = *tag_ctr + 1)
-  uint32_t grid;              // CTAs of the launch (the tagged tail's reset waits for all tickets)
-  int tagged_last;            // A/B: tagged slots, but the last F CTAs out finish (after the grid)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -444,7 +378,7 @@ __device__ __forceinline__ void taper_roots(const FinishArgs& p, uint64_t f, uin
 }
 
 template <class Op>
-__device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm, uint32_t tag = 0) {
+__device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, TreeSmem& sm) {
   const bool send = p.world > 1 && p.early_send;
   if (p.warp_mode) {
     const int lane = threadIdx.x & 31;
@@ -469,10 +403,9 @@ __device__ void segment_values(const FinishArgs& p, uint64_t j, uint64_t F, Tree
       taper_roots<Op>(p, f, n, threadIdx.x, blockDim.x);
       __syncthreads();
     }
-    const float r = n ? cta_tree<Op>(p.partial + f, n, sm, p.troots ? p.troots + f : nullptr, tag) : Op::empty();
+    const float r = n ? cta_tree<Op>(p.partial + f, n, sm) : Op::empty();
     if (threadIdx.x == 0) {
       __stcg(p.out + s, r);
-      if (p.troots) st_relaxed_gpu_u64(p.troots + p.first_item[p.nseg] + s, (uint64_t(tag) << 32) | __float_as_uint(r));
       if (send) send_value(p, s, r);
     }
   }
@@ -491,9 +424,6 @@ __device__ __noinline__ void peer_timeout(const FinishArgs& p) {
   }
 }
 
-template <class Op>
-__device__ __noinline__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag);
-
 // Called by all F finisher CTAs after their segments are written. The last
 // one to arrive resets the counters and runs reduce_cl stage 2: on one GPU
 // directly over the partition values; sharded, it first stores this rank's
@@ -502,32 +432,10 @@ __device__ __noinline__ void stage2_values(const FinishArgs& p, uint32_t F, Tree
 // region (acquire) and runs the same pairing tree over all P values in
 // partition order — the collective fused into the reduction kernel.
 template <class Op>
-__device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag = 0) {
+__device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
   __shared__ bool last;
   const int tid = threadIdx.x;
   __syncthreads();
-  if (p.troots) {
-    // tagged tail: the last finisher runs stage 2 (its partition values are
-    // read through their tags); the counters are reset at the very end,
-    // once every CTA of the grid has taken its exit ticket
-    if (tid == 0) last = atomicAdd(p.done + 1, 1u) == F - 1;
-    __syncthreads();
-    if (!last) return;
-    if (p.result) stage2_values<Op>(p, F, sm, tag);
-    if (tid == 0) {
-      const uint64_t t0 = global_ns();
-      uint32_t spins = 0;
-      while (ld_acquire_gpu(p.done) < p.grid) {
-        __nanosleep(32);
-        if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();  // cooperative: cannot happen
-      }
-      p.done[0] = 0;
-      p.done[1] = 0;
-      p.done[2] = 0;
-      *p.tag_ctr = tag;  // the next launch's tag is tag + 1
-    }
-    return;
-  }
   if (F == 1) {
     // the only finisher wrote every partition value itself: the barrier
     // orders those stores before the reads below, no ticket needed
@@ -551,16 +459,7 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t t
     __threadfence();
   }
   if (!p.result) return;
-  stage2_values<Op>(p, F, sm, 0);
-}
-
-// reduce_cl stage 2 proper: the pairing tree over all partition values in
-// partition order (after the NVLink exchange when sharded) into *p.result.
-// tag != 0: this rank's values are read through the tagged slots.
-template <class Op>
-__device__ __noinline__ void stage2_values(const FinishArgs& p, uint32_t F, TreeSmem& sm, uint32_t tag) {
-  const int tid = threadIdx.x;
-  if (!tag && F == 1 && p.world <= 1 && p.warp_mode && p.nseg && p.nseg <= 32) {
+  if (F == 1 && p.world <= 1 && p.warp_mode && p.nseg && p.nseg <= 32) {
     // stage 2 over <= 32 values from shared memory by warp 0: the padded
     // pairing tree is 5 xor-shuffle levels (lower lane = left operand)
     if (tid < 32) {
@@ -635,9 +534,7 @@ __device__ __noinline__ void stage2_values(const FinishArgs& p, uint32_t F, Tree
     vals = reinterpret_cast<const float*>(p.peers[p.rank]) + buf;
     nvals = p.p_total;
   }
-  // one GPU, tagged tail: this launch's partition values through their tags
-  const uint64_t* tv = tag && p.world <= 1 ? p.troots + p.first_item[p.nseg] : nullptr;
-  const float root = nvals ? cta_tree<Op>(vals, nvals, sm, tv, tag) : Op::empty();
+  const float root = nvals ? cta_tree<Op>(vals, nvals, sm) : Op::empty();
   if (tid == 0) {
     *p.result = root;
     if (p.world > 1) *p.epoch = epoch;
@@ -680,9 +577,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
-  // tagged tail: this launch's tag (the table's launch counter only moves
-  // at the end of a launch, after every CTA has read it)
-  const uint32_t tag = p.fin.troots ? *reinterpret_cast<volatile uint32_t*>(p.fin.tag_ctr) + 1 : 0;
   // A claim covers kPer consecutive items: one for the read+write map stream,
   // two for the read-only reduction, whose items finish twice as fast and
   // would otherwise saturate the single claim counter.
@@ -719,10 +613,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
       const int64_t valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
       const float r =
           work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
-      if (lane == 0) {
-        if (p.fin.troots) st_relaxed_gpu_u64(p.fin.troots + item, (uint64_t(tag) << 32) | __float_as_uint(r));
-        else p.partial[item] = r;
-      }
+      if (lane == 0) p.partial[item] = r;
     }
     unit = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : unit + nwarps;
   }
@@ -733,34 +624,25 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   const uint32_t F = p.fin.finishers ? p.fin.finishers : uint32_t(umin(G, p.fin.nseg ? p.fin.nseg : 1));
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (!p.fin.troots) __threadfence();  // tagged roots need no fence
+    __threadfence();
     ticket = atomicAdd(p.fin.done, 1u);
   }
   __syncthreads();
-  // tagged tail: the FIRST F CTAs out of the stream are the finishers — a
-  // partition's tree starts as soon as its roots carry this launch's tag,
-  // while the grid's last items are still streaming. Ticketed tail (and the
-  // tagged_last A/B): the LAST F CTAs out, once the whole grid has left the
-  // stream. One call site for the partition trees and stage 2 (the kernel's
-  // code size shows in the latency-bound C1 step).
-  const bool early = p.fin.troots && !p.fin.tagged_last;
-  if (early ? ticket >= F : ticket + F < G) return;
-  if (!early) {
-    if (threadIdx.x == 0) {
-      // every CTA is resident (cooperative launch), so the others finish their
-      // stream; a wait of kPeerWaitNs cannot happen — trap rather than reduce
-      // item roots that are not all written
-      const uint64_t t0 = global_ns();
-      uint32_t spins = 0;
-      while (ld_acquire_gpu(p.fin.done) < G) {
-        __nanosleep(32);
-        if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();
-      }
+  if (ticket + F < G) return;
+  if (threadIdx.x == 0) {
+    // every CTA is resident (cooperative launch), so the others finish their
+    // stream; a wait of kPeerWaitNs cannot happen — trap rather than reduce
+    // item roots that are not all written
+    const uint64_t t0 = global_ns();
+    uint32_t spins = 0;
+    while (ld_acquire_gpu(p.fin.done) < G) {
+      __nanosleep(32);
+      if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();
     }
-    __syncthreads();
   }
-  segment_values<Op>(p.fin, early ? ticket : ticket + F - G, F, sm, tag);
-  stage2<Op>(p.fin, F, sm, tag);
+  __syncthreads();
+  segment_values<Op>(p.fin, ticket + F - G, F, sm);
+  stage2<Op>(p.fin, F, sm);
 }
 
 // Stand-alone finish (tables with no work items, or UCG_SEPARATE_FINISH=1):
@@ -1024,9 +906,7 @@ cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = 1;
   }
-  Pass1Args a = args;
-  a.fin.grid = grid;  // the tagged tail's reset waits for every CTA's exit ticket
-  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, a);
+  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, args);
 }
 
 template <class Op, bool kMap>
@@ -1109,19 +989,6 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
       f.warp_mode = 1;
       f.finishers = 1;
     }
-  }
-  // tagged tail: cooperative multi-finisher launches with one CTA per
-  // partition tree (UCG_TAGGED_TAIL=0 restores the ticketed tail for A/B)
-  static const bool tagged_ok = [] {
-    const char* e = getenv("UCG_TAGGED_TAIL");
-    return !e || atoi(e) != 0;
-  }();
-  if (tagged_ok && fused_finish && !f.warp_mode && f.finishers != 1 && !f.ntaper && !f.flag_exchange && t->d_troots &&
-      dynamic_items() && !getenv("UCG_PDL_MULTI")) {
-    f.troots = t->d_troots;
-    f.tag_ctr = t->d_done + 3;
-    static const bool tagged_last = getenv("UCG_TAGGED_LAST") != nullptr;
-    f.tagged_last = tagged_last ? 1 : 0;
   }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,

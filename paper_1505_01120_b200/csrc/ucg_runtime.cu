@@ -358,7 +358,6 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
     cudaFree(t->d_first_item);
     cudaFree(t->d_item_seg);
     cudaFree(t->d_done);
-    cudaFree(t->d_troots);
     delete t;
     return cuda_fail(e, what);
   };
@@ -369,10 +368,6 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_done, 16)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMemset(t->d_done, 0, 16)) != cudaSuccess) return cleanup(e, "cudaMemset");
-  // tagged-tail slots, zero = no launch's tag (tags start at 1)
-  if ((e = cudaMalloc(&t->d_troots, (nitems + nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMemset(t->d_troots, 0, (nitems + nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMemset");
-
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
@@ -394,7 +389,6 @@ int ucg_segtab_destroy(ucg_segtab* t) {
   cudaFree(t->d_first_item);
   cudaFree(t->d_item_seg);
   cudaFree(t->d_done);
-  cudaFree(t->d_troots);
   if (cur >= 0 && cur != t->device) cudaSetDevice(cur);
   delete t;
   return UCG_OK;
