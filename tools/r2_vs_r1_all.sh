@@ -1,0 +1,13 @@
+# same-box comparison of every workload's device value: the round-1 build
+# (build/r1tree, commit 79d596b) against this one
+for rep in 1; do
+  for w in c1 c3 c4 c5 wc; do
+    for t in r1 r2; do
+      if [ $t = r1 ]; then d=build/r1tree; else d=.; fi
+      (cd $d && timeout 600 python bench.py --workload $w --no-cpu-baseline > /tmp/w.json 2>/dev/null || timeout 600 python bench.py --workload $w > /tmp/w.json 2>/dev/null)
+      python -c "
+import json
+d=json.loads(open('/tmp/w.json').read().strip().splitlines()[-1]); print('$t $w rep=$rep', '%.4g' % d['value'], d['unit'], round(d['ms_per_step'],4))" 2>&1 | tail -1
+    done
+  done
+done
