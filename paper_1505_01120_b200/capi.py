@@ -7,6 +7,7 @@ compute call raises.
 """
 from __future__ import annotations
 
+import array
 import ctypes as C
 import os
 from pathlib import Path
@@ -139,10 +140,10 @@ def call(name: str, *args, phase: str = "run") -> None:
 
 
 def u64_array(vals: Sequence[int]) -> C.Array:
-    arr = (C.c_uint64 * max(1, len(vals)))()
-    for i, v in enumerate(vals):
-        arr[i] = int(v)
-    return arr
+    """A C uint64 array of `vals` (negative or > 2^64-1 values raise OverflowError)."""
+    if not len(vals):
+        return (C.c_uint64 * 1)()
+    return (C.c_uint64 * len(vals)).from_buffer_copy(array.array("Q", vals))
 
 
 def ptr(x) -> int | None:

@@ -209,8 +209,13 @@ def sobel_bands(inp, in_off: Sequence[int], out, out_off: Sequence[int], rows: S
     _dtype(out, torch.uint8, "out")
     if not (len(in_off) == len(out_off) == len(rows)):
         raise ValueError("one input offset, output offset and row count per band")
-    _at_least(inp, max((o + (r + 2) * width for o, r in zip(in_off, rows)), default=0), "inp")
-    _at_least(out, max((o + r * width for o, r in zip(out_off, rows)), default=0), "out")
+    if rows:  # the last band ends furthest when bands are laid out in order (the common case: check it first)
+        in_end = in_off[-1] + (rows[-1] + 2) * width
+        out_end = out_off[-1] + rows[-1] * width
+        if in_end > inp.numel() or out_end > out.numel() or any(
+                b < a for a, b in zip(in_off, in_off[1:])) or any(b < a for a, b in zip(out_off, out_off[1:])):
+            _at_least(inp, max(o + (r + 2) * width for o, r in zip(in_off, rows)), "inp")
+            _at_least(out, max(o + r * width for o, r in zip(out_off, rows)), "out")
     call("ucg_sobel_bands_u8", ptr(inp), u64_array(in_off), ptr(out), u64_array(out_off), u64_array(rows),
          len(rows), width, stream_handle(stream))
     return out
