@@ -127,8 +127,7 @@ struct ucg_segtab {
   uint32_t* d_item_seg;    // [nitems]
   uint64_t max_items_per_seg;
   int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
-  uint32_t* d_done;        // [8] pass-1 exit / finisher / item counters, [4..8) the A/B multi-counter
-                           // claims (zero between launches)
+  uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches)
   uint64_t ntaper;         // trailing items the fused map streams as 4 sub-items each (0: none)
 };
 

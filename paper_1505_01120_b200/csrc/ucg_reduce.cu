@@ -294,7 +294,6 @@ struct FinishArgs {
                               // values as it computes them (stage 2 only receives)
   float* sub;                 // tapered tail: 4 sub-item roots per item in [taper_first, +ntaper)
   uint64_t taper_first, ntaper;
-  int multi_claim;            // pass 1 claimed from the counters done[4..8) (reset them too)
 };
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
@@ -444,7 +443,6 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
       p.done[0] = 0;
       p.done[1] = 0;
       p.done[2] = 0;
-      if (p.multi_claim) p.done[4] = p.done[5] = p.done[6] = p.done[7] = 0;
     }
   } else {
     if (tid == 0) {
@@ -457,7 +455,6 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
       p.done[0] = 0;
       p.done[1] = 0;
       p.done[2] = 0;
-      if (p.multi_claim) p.done[4] = p.done[5] = p.done[6] = p.done[7] = 0;
     }
     __threadfence();
   }
@@ -569,15 +566,7 @@ struct Pass1Args {
   FinishArgs fin;
 };
 
-// kCtr > 1 (A/B, UCG_CLAIM_COUNTERS): units are claimed from kCtr counters
-// (fin.done[4..4+kCtr)), counter c handing out units nwarps + c + kCtr*j;
-// warp w starts on counter w % kCtr and moves to the next counters once its
-// own is exhausted — kCtr times the claim rate of one counter.
-// kXPre (A/B, UCG_CROSS_PREFETCH=1; fused map with claimed items): the next
-// item's first chunk is loaded while the current item's last chunk is
-// mapped and reduced (the claim issued at the item's start has returned by
-// then), so a warp's pipeline does not restart at every item boundary.
-template <class Op, bool kMap, int U, int kMinBlocks, int kCtr = 1, bool kXPre = false>
+template <class Op, bool kMap, int U, int kMinBlocks>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const __grid_constant__ Pass1Args p) {
   // Programmatic dependent launch (small tables, see launch_pass1): this grid
   // may be resident before the previous step's grid has finished; wait for it
@@ -597,73 +586,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   const uint64_t ntaper = kMap ? p.fin.ntaper : 0;
   const uint64_t units_end = ntaper ? p.fin.taper_first + 4 * ntaper : 0;
   uint64_t unit = warp;
-  uint32_t cidx = kCtr > 1 ? uint32_t(warp % kCtr) : 0;
-  if constexpr (kXPre && kMap) {
-    // whole items, one chunk ahead across item boundaries
-    constexpr int kChunk = 128 * U;
-    constexpr int kMaxChunks = int((1ull << kMaxItemLog2) / kChunk);
-    constexpr int kDepth = (kMaxChunks >= 64 ? 6 : kMaxChunks >= 32 ? 5 : kMaxChunks >= 16 ? 4 : kMaxChunks >= 8 ? 3 : 2);
-    const int64_t item_floats = int64_t(1) << p.item_log2;
-    const int kChunks = int(item_floats / kChunk);
-    auto locate = [&](uint64_t item, uint64_t& off, int64_t& valid) {
-      const uint32_t s = p.item_seg[item];
-      const uint64_t blk = item - p.first_item[s];
-      off = p.begin[s] + (blk << p.item_log2);
-      valid = int64_t(umin(uint64_t(item_floats), p.len[s] - (blk << p.item_log2)));
-    };
-    float4 cur[U];
-    bool have = false;  // cur holds chunk 0 of `unit`
-    while (unit < p.nitems) {
-      uint32_t claim = 0;
-      if (lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
-      uint64_t off;
-      int64_t valid;
-      locate(unit, off, valid);
-      uint64_t next = 0;
-      float r;
-      if (valid < item_floats) {  // a segment's partial last item: the plain path
-        r = work_item<Op, true, U>(p.x + off, p.y + off, valid, item_floats, p.a, p.b, lane);
-        next = nwarps + __shfl_sync(kFull, claim, 0);
-        have = false;
-      } else {
-        if (!have) chunk_load<Op, false, U>(p.x + off, kChunk, lane, cur);
-        float stk[kDepth];
-#pragma unroll
-        for (int j = 0; j < kDepth; ++j) stk[j] = Op::identity();
-        float v = Op::identity();
-        have = false;
-#pragma unroll 1
-        for (int c = 0; c < kChunks; ++c) {
-          float4 nxt[U];
-          if (c + 1 < kChunks) {
-            chunk_load<Op, false, U>(p.x + off + (c + 1) * kChunk, kChunk, lane, nxt);
-          } else {
-            next = nwarps + __shfl_sync(kFull, claim, 0);
-            if (next < p.nitems) {
-              uint64_t noff;
-              int64_t nvalid;
-              locate(next, noff, nvalid);
-              if (nvalid >= item_floats) {
-                chunk_load<Op, false, U>(p.x + noff, kChunk, lane, nxt);
-                have = true;
-              }
-            }
-          }
-          v = chunk_finish<Op, true, false, U>(cur, p.y + off + c * kChunk, kChunk, p.a, p.b, lane);
-          counter_push<Op, kDepth>(stk, v, c);
-#pragma unroll
-          for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-        }
-        r = v;  // c = kChunks-1 has all bits set: v is the root
-      }
-      if (lane == 0) p.partial[unit] = r;
-      unit = next;
-    }
-  } else
   while (ntaper ? unit < units_end : unit * kPer < p.nitems) {
     // dynamic: the next unit is claimed now and consumed after this one
     uint32_t claim = 0;
-    if (p.dynamic && lane == 0) claim = atomicAdd(kCtr > 1 ? p.fin.done + 4 + cidx : p.fin.done + 2, 1u);
+    if (p.dynamic && lane == 0) claim = atomicAdd(p.fin.done + 2, 1u);
     if (ntaper && unit >= p.fin.taper_first) {
       const uint64_t u = unit - p.fin.taper_first, item = p.fin.taper_first + (u >> 2);
       const uint32_t s = p.item_seg[item];
@@ -688,20 +614,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
       const float r =
           work_item<Op, kMap, U>(p.x + off, kMap ? p.y + off : nullptr, valid, item_floats, p.a, p.b, lane);
       if (lane == 0) p.partial[item] = r;
-    }
-    if constexpr (kCtr > 1) {
-      if (p.dynamic) {
-        unit = nwarps + cidx + uint64_t(kCtr) * __shfl_sync(kFull, claim, 0);
-        // this counter is exhausted: take the next ones' remaining units
-#pragma unroll 1
-        for (int t = 1; t < kCtr && unit * kPer >= p.nitems; ++t) {
-          cidx = (cidx + 1) % kCtr;
-          uint32_t c2 = 0;
-          if (lane == 0) c2 = atomicAdd(p.fin.done + 4 + cidx, 1u);
-          unit = nwarps + cidx + uint64_t(kCtr) * __shfl_sync(kFull, c2, 0);
-        }
-        continue;
-      }
     }
     unit = p.dynamic ? nwarps + __shfl_sync(kFull, claim, 0) : unit + nwarps;
   }
@@ -964,7 +876,7 @@ inline int pass1_variant() {
   return v;
 }
 
-template <class Op, bool kMap, int U, int MINB, int kCtr = 1, bool kXPre = false>
+template <class Op, bool kMap, int U, int MINB>
 cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_t st) {
   const uint64_t want = (t->nitems + kWarps - 1) / kWarps;
   const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sm_count()) * MINB)));
@@ -994,7 +906,7 @@ cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = 1;
   }
-  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB, kCtr, kXPre>, args);
+  return cudaLaunchKernelEx(&cfg, k_segment_pass1<Op, kMap, U, MINB>, args);
 }
 
 template <class Op, bool kMap>
@@ -1005,16 +917,7 @@ cudaError_t dispatch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStrea
     case 3: return launch_pass1<Op, kMap, 2, 8>(args, t, st);
     case 4: return launch_pass1<Op, kMap, 2, 6>(args, t, st);
     case 5: return launch_pass1<Op, kMap, 8, 3>(args, t, st);
-    default:
-      if (args.fin.multi_claim) return launch_pass1<Op, kMap, 8, 2, 4>(args, t, st);
-      if constexpr (kMap) {
-        static const bool xpre = [] {
-          const char* e = getenv("UCG_CROSS_PREFETCH");
-          return e && atoi(e) != 0;
-        }();
-        if (xpre && args.dynamic && !args.fin.ntaper) return launch_pass1<Op, kMap, 8, 2, 1, true>(args, t, st);
-      }
-      return launch_pass1<Op, kMap, 8, 2>(args, t, st);
+    default: return launch_pass1<Op, kMap, 8, 2>(args, t, st);
   }
 }
 
@@ -1087,12 +990,6 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
       f.finishers = 1;
     }
   }
-  // A/B: four claim counters (UCG_CLAIM_COUNTERS=4, default variant, claimed items, no taper)
-  static const bool multi_claim = [] {
-    const char* e = getenv("UCG_CLAIM_COUNTERS");
-    return e && atoi(e) == 4;
-  }();
-  f.multi_claim = multi_claim && pass1_variant() == kPass1Default && dynamic_items() && !f.ntaper ? 1 : 0;
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
                    a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, f};

@@ -366,8 +366,8 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if ((e = cudaMalloc(&t->d_len, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_first_item, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMalloc(&t->d_done, 32)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMemset(t->d_done, 0, 32)) != cudaSuccess) return cleanup(e, "cudaMemset");
+  if ((e = cudaMalloc(&t->d_done, 16)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMemset(t->d_done, 0, 16)) != cudaSuccess) return cleanup(e, "cudaMemset");
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
