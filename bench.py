@@ -83,6 +83,8 @@ def parse():
                     help="c2 (default) is the headline; the others are the remaining BASELINE configs")
     ap.add_argument("--cpu-sample-parts", type=int, default=4,
                     help="partitions in our arm's bounded cpu_baseline sample")
+    ap.add_argument("--ref-steps", type=int, default=8,
+                    help="--impl reference: at most this many timed steps (each is the whole workload on the CPU)")
     ap.add_argument("--ref-parts", type=int, default=0,
                     help="--impl reference: partitions timed (default 0 = the whole --parts workload)")
     return ap.parse_args()
@@ -163,7 +165,12 @@ def reference_arm(args, world, rank):
         return 0
     threads = os.cpu_count() or 1
     parts = args.ref_parts or args.parts
-    r = run_ref_harness(parts, args.part_len, args.steps, args.warmup, args.op, threads)
+    # one CPU step over the whole workload takes ~15 s, so the arm times at
+    # most --ref-steps (default 8) of the K steps after one warm-up step (a
+    # CPU path has no clocks or caches to warm beyond faulting in its heap):
+    # ~2.5 min instead of 25 x 15 s; the line states both counts
+    steps, warmup = min(args.steps, args.ref_steps), min(args.warmup, 1)
+    r = run_ref_harness(parts, args.part_len, steps, warmup, args.op, threads)
     elems = r["elements"]
     step = statistics.fmean(r["step_s"])
     value = elems / step
@@ -175,7 +182,8 @@ def reference_arm(args, world, rank):
               f"{cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": cfg,
         "reference_path": "unmodified ucores Engine + WorkerRuntime + HostParallelExecutor (oracle/_ref/ref_harness, "

@@ -40,6 +40,22 @@ def _timed(fn, k, barrier):
     return e0.elapsed_time(e1) / k
 
 
+def _soak(fn, warmup, barrier, seconds=1.0):
+    """Inside the clock sampler, before a timed region: W warm-up calls, then
+    ~1 s of untimed calls, so nvidia-smi is up and sampling (its start-up
+    no longer overlaps a few-ms timed region) and the clocks are at steady
+    state — as bench.py's C2 arm does."""
+    for _ in range(max(3, warmup)):
+        fn()
+    barrier()
+    end = time.perf_counter() + seconds
+    while time.perf_counter() < end:
+        for _ in range(10):
+            fn()
+        torch.cuda.synchronize()
+    barrier()
+
+
 def _max_over_ranks(vals, world, dev):
     if world == 1:
         return vals
@@ -107,6 +123,7 @@ def run(args, world, rank, local):
             pipe.graph_step()
         pipe.graph_step(k)  # capture + warm replay
         with B.ClockSampler(local) as clk:
+            _soak(pipe.graph_step, w, barrier)
             ms = _timed(lambda: pipe.graph_step(k), 1, barrier) / k
             launches = k  # one k_segment_pass1 node per step (graph replays bypass the C launch counter)
             kern = _timed(pipe.map_and_partials, k, barrier)
@@ -159,6 +176,7 @@ def run(args, world, rank, local):
             ops.pi_hits(seeds, samples, hits, total_out=total, xchg=xg)
         fn()
         with B.ClockSampler(local) as clk:
+            _soak(fn, args.warmup, barrier)
             l0 = capi.launch_count()
             ms = _timed(fn, k, barrier)
             launches = capi.launch_count() - l0
@@ -208,6 +226,7 @@ def run(args, world, rank, local):
         fn = lambda: ops.sobel_bands(inp, in_off, out, out_off, [R] * ln, W)
         fn()
         with B.ClockSampler(local) as clk:
+            _soak(fn, args.warmup, barrier)
             l0 = capi.launch_count()
             ms = _timed(fn, k, barrier)
             launches = capi.launch_count() - l0
@@ -259,6 +278,7 @@ def run(args, world, rank, local):
         fn32()
         fntf()
         with B.ClockSampler(local) as clk:
+            _soak(fn32, args.warmup, barrier)
             l0 = capi.launch_count()
             ms32 = _timed(fn32, k, barrier)
             launches = capi.launch_count() - l0  # split x2 + GEMM per partition
@@ -388,6 +408,7 @@ def run(args, world, rank, local):
         fn = lambda: ops.word_start_flags(text, flags)
         fn()
         with B.ClockSampler(local) as clk:
+            _soak(fn, args.warmup, barrier)
             l0 = capi.launch_count()
             ms = _timed(fn, k, barrier)
             launches = capi.launch_count() - l0

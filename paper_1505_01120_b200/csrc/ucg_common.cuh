@@ -35,6 +35,12 @@ extern std::atomic<uint64_t> g_launches;
 // cannot be allocated.
 unsigned long long* claim_counter();
 
+// A {claims, exit tickets} pair of 8-byte counters for a kernel that resets
+// them itself (the last CTA to exit zeroes both), from a ring zeroed once at
+// allocation: no memset launch before each use. Null if the ring cannot be
+// allocated.
+unsigned long long* claim_pair_selfreset();
+
 // True the first time it is called on the current device for this flag word.
 // Kernel attributes (cudaFuncSetAttribute) are per device: a process driving
 // several GPUs (the seam-A driver) must set them on each one.

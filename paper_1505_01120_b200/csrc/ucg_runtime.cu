@@ -104,6 +104,28 @@ unsigned long long* claim_counter() {
   return ring[d] + (next[d]++ % kSlots);
 }
 
+unsigned long long* claim_pair_selfreset() {
+  // every user of this ring leaves its pair at zero when its launch ends, so
+  // a slot handed out again (after 2^15 later launches) is clean
+  constexpr uint64_t kPairs = 1u << 15;
+  static std::mutex mu;
+  static unsigned long long* ring[64] = {};
+  static uint64_t next[64] = {};
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ring[d]) {
+    unsigned long long* r = nullptr;
+    if (cudaMalloc(&r, kPairs * 2 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    if (cudaMemset(r, 0, kPairs * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaFree(r);
+      return nullptr;
+    }
+    ring[d] = r;
+  }
+  return ring[d] + 2 * (next[d]++ % kPairs);
+}
+
 int sm_count() {
   int dev = -1;
   const DevCache* c = dev_cache(&dev);

@@ -12,10 +12,12 @@
 // 3-row window in registers, so each input row is read from HBM once (plus
 // 2 halo rows per strip); the left/right neighbour bytes come from the
 // adjacent lanes by shuffle. One 128-bit store per output row.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "ucg_common.cuh"
@@ -198,6 +200,72 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
   return d;
 }
 
+// ---- the per-pixel arithmetic, two forms ----------------------------------------
+// Both work on even/odd planes of packed 16-bit halves (E = pixels 4k, 4k+2;
+// O = 4k+1, 4k+3; Le / Ro = the left neighbours of the even pixels and the
+// right neighbours of the odd ones).
+//
+// kHalf (UCG_SOBEL_ARITH=half): each 16-bit half holding a byte p is read as the fp16
+// SUBNORMAL p * 2^-24. Every intermediate (dh, sh, Gx, Gy, |Gx|+|Gy|) is an
+// integer multiple of 2^-24 of magnitude <= 2040 < 2048, so HADD2/HFMA2 are
+// exact; |.| is a free operand modifier of HADD2, the clamp is one HMNMX2 and
+// min(|Gx|+|Gy|, 255) * 2^-24 has the output byte as its low byte. The work
+// lands on the FMA pipe (HADD2/HFMA2), leaving the ALU pipe the byte permutes.
+// Integer form (default): biased u16x2 lanes, IMAD on the FMA pipe and
+// VIMNMX/IADD3 on the ALU pipe. The fp16 form moves the arithmetic off the
+// ALU pipe onto the fp16 pipe, which runs at the same half rate; it measured
+// no faster.
+__device__ __forceinline__ __half2 h2_of(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return h;
+}
+__device__ __forceinline__ uint32_t u_of(__half2 h) {
+  uint32_t u;
+  memcpy(&u, &h, 4);
+  return u;
+}
+
+// row terms of one 4-pixel word: dh = R - L, sh = L + 2C + R for the even and
+// the odd plane (integer form: unbiased, exact mod 2^32 on the packed word)
+template <bool kHalf>
+__device__ __forceinline__ void word_terms(uint32_t E, uint32_t O, uint32_t Le, uint32_t Ro, uint32_t one,
+                                           uint32_t two, uint32_t m1, uint32_t& dhe, uint32_t& dho, uint32_t& she,
+                                           uint32_t& sho) {
+  if constexpr (kHalf) {
+    const __half2 e = h2_of(E), o = h2_of(O), l = h2_of(Le), r = h2_of(Ro), k2 = __float2half2_rn(2.f);
+    dhe = u_of(__hsub2(o, l));
+    dho = u_of(__hsub2(r, e));
+    she = u_of(__hfma2(e, k2, __hadd2(l, o)));
+    sho = u_of(__hfma2(o, k2, __hadd2(e, r)));
+  } else {
+    dhe = mad_u32(Le, m1, O);
+    dho = mad_u32(E, m1, Ro);
+    she = mad_u32(E, two, mad_u32(Le, one, O));
+    sho = mad_u32(O, two, mad_u32(E, one, Ro));
+  }
+}
+
+// one packed output pair from input rows (a, b, c) = (r, r+1, r+2); the
+// output bytes are the low bytes of the two halves
+template <bool kHalf>
+__device__ __forceinline__ uint32_t out_pair(uint32_t adh, uint32_t bdh, uint32_t cdh, uint32_t ash, uint32_t csh,
+                                             uint32_t two, uint32_t m1) {
+  if constexpr (kHalf) {
+    const __half2 gx = __hfma2(h2_of(bdh), __float2half2_rn(2.f), __hadd2(h2_of(adh), h2_of(cdh)));
+    const __half2 gy = __hsub2(h2_of(csh), h2_of(ash));
+    return u_of(__hmin2(__hadd2(__habs2(gx), __habs2(gy)), h2_of(0x00FF00FFu)));
+  } else {
+    // per half: gx' = Gx + 1024, gy' = Gy + 1024, both in [4, 2044]
+    const uint32_t gx = mad_u32(bdh, two, adh + cdh + 0x04000400u);
+    const uint32_t gy = csh - ash + 0x04000400u;
+    // |G| + 1024 = max(g', 2048 - g') per half
+    const uint32_t ax = __vmaxu2(gx, mad_u32(gx, m1, 0x08000800u));
+    const uint32_t ay = __vmaxu2(gy, mad_u32(gy, m1, 0x08000800u));
+    return __vminu2(__vadd2(ax, ay), 0x08FF08FFu);  // min(|Gx|+|Gy|, 255) + 2048
+  }
+}
+
 __device__ __forceinline__ void tile_of(const SobelTiles& p, uint32_t t, uint32_t& b, uint32_t& rb, uint32_t& cb) {
   uint32_t lo = 0, hi = p.nbands;
   while (hi - lo > 1) {
@@ -220,14 +288,21 @@ struct SobelMaps {
 // and published to the CTA by the buffer's mbarrier phase (the arrive has
 // release semantics), so only that thread runs the band search.
 struct TileInfo {
-  uint32_t b, rb, cb;
+  uint32_t b, rb, cb, valid;
 };
 
 __device__ __forceinline__ void issue_tile(const SobelMaps* maps, const SobelTiles& p, uint32_t t, uint8_t* buf,
                                            uint64_t* bar, TileInfo* info) {
+  if (t >= p.first_tile[p.nbands]) {
+    // no tile left: complete the buffer's phase with a plain arrive, so the
+    // consumers wake up, see valid == 0 and leave
+    *info = TileInfo{0, 0, 0, 0};
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(bar)) : "memory");
+    return;
+  }
   uint32_t b, rb, cb;
   tile_of(p, t, b, rb, cb);
-  *info = TileInfo{b, rb, cb};
+  *info = TileInfo{b, rb, cb, 1};
   const int x = int(cb) * kTW, y = int(p.in_row0[b] + rb * kTH);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)),
                "r"(kCenterBytes + 2 * kSideBytes) : "memory");
@@ -241,9 +316,10 @@ __device__ __forceinline__ void issue_tile(const SobelMaps* maps, const SobelTil
         : "memory");
 }
 
+template <bool kHalf>
 __global__ void __launch_bounds__(kTmaThreads)
     k_sobel_tma(const __grid_constant__ SobelMaps maps, uint8_t* __restrict__ out, const __grid_constant__ SobelTiles p,
-                uint64_t width, uint32_t ntiles) {
+                uint64_t width, unsigned long long* __restrict__ ctr) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   __shared__ __align__(8) uint64_t full[2];
@@ -258,16 +334,31 @@ __global__ void __launch_bounds__(kTmaThreads)
   __syncthreads();
   uint32_t it = 0;
   if (tid == 0) {
-    if (blockIdx.x < ntiles) issue_tile(map, p, blockIdx.x, smem, &full[0], &info[0]);
-    if (blockIdx.x + gridDim.x < ntiles)
-      issue_tile(map, p, blockIdx.x + gridDim.x, smem + kBufBytes, &full[1], &info[1]);
+    issue_tile(map, p, blockIdx.x, smem, &full[0], &info[0]);
+    issue_tile(map, p, blockIdx.x + gridDim.x, smem + kBufBytes, &full[1], &info[1]);
   }
-  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+  // Tiles after the first two per CTA: claimed from a counter (ctr[0]) when a
+  // buffer frees up, so SMs that run ahead take more tiles and the grid ends
+  // together; ctr == null: the static round-robin t += gridDim.x. Claims only
+  // grow, so the first empty buffer ends the CTA with no copy in flight.
+  uint32_t t = blockIdx.x;
+  for (;; ++it) {
     const uint32_t bi = it & 1;
     uint8_t* buf = smem + bi * kBufBytes;
     asm volatile("{\n .reg .pred q;\n W:\n mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n @!q bra W;\n}\n" ::"r"(
                      sa(&full[bi])), "r"((it >> 1) & 1)
                  : "memory");
+    if (!info[bi].valid) {
+      // the last CTA out returns the claim pair to zero for its next user
+      if (ctr && tid == 0) {
+        __threadfence();
+        if (atomicAdd(ctr + 1, 1ull) == gridDim.x - 1) {
+          ctr[0] = 0;
+          ctr[1] = 0;
+        }
+      }
+      break;
+    }
     const uint32_t b = info[bi].b, rb = info[bi].rb, cb = info[bi].cb;
     const uint32_t valid_rows = min(uint32_t(kTH), p.rows[b] - rb * kTH);
     const uint64_t col = uint64_t(cb) * kTW + cg * 16;
@@ -310,10 +401,8 @@ __global__ void __launch_bounds__(kTmaThreads)
         // left of the even pixels (p[4k-1], p[4k+1]); right of the odd ones (p[4k+2], p[4k+4])
         const uint32_t Le = k ? __byte_perm(O[k - 1], O[k], 0x5432) : __byte_perm(pw, O[0], 0x5453);
         const uint32_t Ro = k < 3 ? __byte_perm(E[k], E[k + 1], 0x5432) : __byte_perm(E[3], nw, 0x1432);
-        tr.dh[2 * k] = mad_u32(Le, m1, O[k]);                 // R - L, even
-        tr.dh[2 * k + 1] = mad_u32(E[k], m1, Ro);             // R - L, odd
-        tr.sh[2 * k] = mad_u32(E[k], two, mad_u32(Le, one, O[k]));      // L + 2C + R, even
-        tr.sh[2 * k + 1] = mad_u32(O[k], two, mad_u32(E[k], one, Ro));  // L + 2C + R, odd
+        word_terms<kHalf>(E[k], O[k], Le, Ro, one, two, m1, tr.dh[2 * k], tr.dh[2 * k + 1], tr.sh[2 * k],
+                          tr.sh[2 * k + 1]);
       }
     };
     uint8_t* dst = out + p.out_off[b] + (uint64_t(rb) * kTH + rg * 8) * width + col;
@@ -321,13 +410,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       if (uint32_t(rg * 8 + r) >= valid_rows || col >= width) return;
       uint32_t o[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t gx = mad_u32(bb.dh[i], two, a.dh[i] + c.dh[i] + 0x04000400u);  // Gx + 1024 per half
-        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;                            // Gy + 1024 per half
-        const uint32_t ax = __vmaxu2(gx, mad_u32(gx, m1, 0x08000800u));
-        const uint32_t ay = __vmaxu2(gy, mad_u32(gy, m1, 0x08000800u));
-        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);  // min(|Gx|+|Gy|, 255) + 2048
-      }
+      for (int i = 0; i < 8; ++i) o[i] = out_pair<kHalf>(a.dh[i], bb.dh[i], c.dh[i], a.sh[i], c.sh[i], two, m1);
       // interleave the planes back: bytes (even lo, odd lo, even hi, odd hi)
       const uint32_t q0 = __byte_perm(o[0], o[1], 0x6240), q1 = __byte_perm(o[2], o[3], 0x6240);
       const uint32_t q2 = __byte_perm(o[4], o[5], 0x6240), q3 = __byte_perm(o[6], o[7], 0x6240);
@@ -355,7 +438,10 @@ __global__ void __launch_bounds__(kTmaThreads)
     terms(i0 + 9, t0);
     emit(7, t1, t2, t0);
     __syncthreads();  // buffer bi fully read
-    if (tid == 0 && t + 2 * gridDim.x < ntiles) issue_tile(map, p, t + 2 * gridDim.x, buf, &full[bi], &info[bi]);
+    if (tid == 0) {
+      t = ctr ? 2 * gridDim.x + uint32_t(atomicAdd(ctr, 1ull)) : t + gridDim.x;
+      issue_tile(map, p, ctr ? t : t + gridDim.x, buf, &full[bi], &info[bi]);
+    }
   }
 }
 
@@ -400,7 +486,7 @@ struct SobelRows {
   uint32_t mul[3];                    // {1, 2, 0xFFFFFFFF}, opaque to the compiler
 };
 
-template <int kMinBlocks, int kSlots, int kCols>
+template <int kMinBlocks, int kSlots, int kCols, bool kHalf>
 __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
     k_sobel_rows(const __grid_constant__ CUtensorMap rows3, uint8_t* __restrict__ out,
                  const __grid_constant__ SobelRows p, uint64_t width) {
@@ -483,22 +569,14 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
       for (int kk = 0; kk < kW; ++kk) {
         const uint32_t Le = kk ? __byte_perm(O[kk - 1], O[kk], 0x5432) : __byte_perm(pw, O[0], 0x5453);
         const uint32_t Ro = kk < kW - 1 ? __byte_perm(E[kk], E[kk + 1], 0x5432) : __byte_perm(E[kW - 1], nw2, 0x1432);
-        tr.dh[2 * kk] = mad_u32(Le, m1, O[kk]);
-        tr.dh[2 * kk + 1] = mad_u32(E[kk], m1, Ro);
-        tr.sh[2 * kk] = mad_u32(E[kk], two, mad_u32(Le, one, O[kk]));
-        tr.sh[2 * kk + 1] = mad_u32(O[kk], two, mad_u32(E[kk], one, Ro));
+        word_terms<kHalf>(E[kk], O[kk], Le, Ro, one, two, m1, tr.dh[2 * kk], tr.dh[2 * kk + 1], tr.sh[2 * kk],
+                          tr.sh[2 * kk + 1]);
       }
     };
     auto emit = [&](uint32_t r, const RowTermsW<kW>& a, const RowTermsW<kW>& bb, const RowTermsW<kW>& c) {
       uint32_t o[2 * kW];
 #pragma unroll
-      for (int i = 0; i < 2 * kW; ++i) {
-        const uint32_t gx = mad_u32(bb.dh[i], two, a.dh[i] + c.dh[i] + 0x04000400u);
-        const uint32_t gy = c.sh[i] - a.sh[i] + 0x04000400u;
-        const uint32_t ax = __vmaxu2(gx, mad_u32(gx, m1, 0x08000800u));
-        const uint32_t ay = __vmaxu2(gy, mad_u32(gy, m1, 0x08000800u));
-        o[i] = __vminu2(__vadd2(ax, ay), 0x08FF08FFu);
-      }
+      for (int i = 0; i < 2 * kW; ++i) o[i] = out_pair<kHalf>(a.dh[i], bb.dh[i], c.dh[i], a.sh[i], c.sh[i], two, m1);
       if (active) {
         uint32_t x[kW];
 #pragma unroll
@@ -597,6 +675,13 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
     const char* e = getenv("UCG_SOBEL_VARIANT");
     return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 1);
   }();
+  // UCG_SOBEL_ARITH=half (A/B runs): the fp16-subnormal arithmetic instead of
+  // the integer form (measured: 98.8 vs 100.7 us alone under ncu, but 110 vs
+  // 99 us back to back — the fp16 pipe is half rate like the ALU pipe)
+  static const bool half_arith = [] {
+    const char* e = getenv("UCG_SOBEL_ARITH");
+    return e && strcmp(e, "half") == 0;
+  }();
   bool rows_ok = vec && variant == 0 && width < (1ull << 31);
   for (uint64_t i = 0; i < nbands && rows_ok; ++i) rows_ok = in_off[i] % width == 0;
   if (rows_ok) {
@@ -610,8 +695,10 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       const char* e = getenv("UCG_SOBEL_SLOTS");
       return e && atoi(e) == 6 ? 6 : 4;
     }();
-    auto kern = cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16> : k_sobel_rows<5, 4, 16>)
-                           : (slots == 6 ? k_sobel_rows<8, 6, 8> : k_sobel_rows<8, 4, 8>);
+    auto kern = half_arith ? (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, true> : k_sobel_rows<5, 4, 16, true>)
+                                         : (slots == 6 ? k_sobel_rows<8, 6, 8, true> : k_sobel_rows<8, 4, 8, true>))
+                           : (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, false> : k_sobel_rows<5, 4, 16, false>)
+                                         : (slots == 6 ? k_sobel_rows<8, 6, 8, false> : k_sobel_rows<8, 4, 8, false>));
     const uint32_t smem = cols == 16 ? (slots == 6 ? sobel_rows_smem<6, 16>() : sobel_rows_smem<4, 16>())
                                      : (slots == 6 ? sobel_rows_smem<6, 8>() : sobel_rows_smem<4, 8>());
     const uint32_t seg_cols = 32u * uint32_t(cols);
@@ -689,9 +776,10 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) return fail(UCG_ERR_CUDA, "sobel tensor map encode failed");
+    auto tkern = half_arith ? k_sobel_tma<true> : k_sobel_tma<false>;
     static std::atomic<uint64_t> attr{0};
     if (first_on_device(attr))
-      UCG_CUDA(cudaFuncSetAttribute(k_sobel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * kBufBytes + 128)));
+      UCG_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * kBufBytes + 128)));
     const uint32_t col_tiles = uint32_t((width + kTW - 1) / kTW);
     for (uint64_t b0 = 0; b0 < nbands; b0 += kMaxBands) {
       const uint32_t nb = uint32_t(std::min<uint64_t>(kMaxBands, nbands - b0));
@@ -711,7 +799,14 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       const uint32_t ntiles = p.first_tile[nb];
       if (!ntiles) continue;
       const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count()) * 5));
-      k_sobel_tma<<<grid, kTmaThreads, 2 * kBufBytes + 128, st>>>(maps, out, p, width, ntiles);
+      // UCG_SOBEL_STATIC (A/B runs): round-robin tiles instead of claimed ones
+      static const bool static_tiles = getenv("UCG_SOBEL_STATIC") != nullptr;
+      unsigned long long* ctr = nullptr;
+      if (!static_tiles) {
+        ctr = claim_pair_selfreset();  // zero at launch; the kernel's last CTA re-zeroes it
+        if (!ctr) return fail(UCG_ERR_CUDA, "sobel: claim counter unavailable");
+      }
+      tkern<<<grid, kTmaThreads, 2 * kBufBytes + 128, st>>>(maps, out, p, width, ctr);
       UCG_LAUNCHED();
     }
     return UCG_OK;

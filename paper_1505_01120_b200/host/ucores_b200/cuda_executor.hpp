@@ -23,6 +23,7 @@
 #include "ucores/worker.hpp"
 #include "ucores_b200/device_ops.hpp"
 #include "ucores_b200/gpu_context.hpp"
+#include "ucores_b200/trace.hpp"
 
 namespace ucores_b200 {
 
@@ -64,6 +65,7 @@ class CudaExecutor : public ucores::KernelExecutor {
       throw ucores::KernelPanic("run", "no device body for kernel '" + name + "' (the GPU path has no CPU fallback)");
     }
     if (ctx.range().global_size == 0) return;
+    TraceRange trace("ucores.run " + name);
     std::lock_guard<std::mutex> lock(gpu_->mutex());
     DeviceGuard guard;
     gpu_->bind();

@@ -40,6 +40,7 @@
 #include <vector>
 
 #include "ucores/dataset.hpp"
+#include "ucores_b200/trace.hpp"
 #include "ucores/element.hpp"
 #include "ucores/errors.hpp"
 #include "ucores_b200/device_ops.hpp"
@@ -202,6 +203,7 @@ class DeviceEngine {
   /// Host Dataset -> HBM. Each partition must hold one element kind (a
   /// partition's bytes are its concatenation); tables stay on the host.
   DeviceDataset upload(const ucores::Dataset& d) {
+    TraceRange trace("ucores.upload");
     std::vector<DevicePartition> parts(d.partition_count());
     for (std::size_t p = 0; p < parts.size(); ++p) {
       const auto& els = d.partitions()[p].elements;
@@ -252,6 +254,7 @@ class DeviceEngine {
   /// partitions. The caller's arrays may be reused once this returns.
   DeviceDataset create_dataset(const std::vector<std::span<const std::uint8_t>>& elements, ucores::ElementKind kind,
                                std::size_t num_partitions) {
+    TraceRange trace("ucores.create_dataset");
     if (num_partitions < 1)
       throw ucores::InvalidPartitionCount("num_partitions must be >= 1, got " + std::to_string(num_partitions));
     const std::size_t eb = entry_bytes(kind), n = elements.size();
@@ -290,6 +293,7 @@ class DeviceEngine {
 
   /// HBM -> host Dataset (the lazy collect of SURVEY §8(f)1).
   ucores::Dataset collect(const DeviceDataset& d) {
+    TraceRange trace("ucores.collect");
     std::vector<ucores::Partition> parts(d.partition_count());
     std::vector<std::vector<std::uint8_t>> staging(d.partition_count());
     for (std::size_t p = 0; p < parts.size(); ++p) {
@@ -313,12 +317,16 @@ class DeviceEngine {
   }
 
   /// Engine::map_cl (engine.hpp:54-85): axpb, psum, pmax, pi, sobel, matmul.
-  DeviceDataset map_cl(const DeviceDataset& d, const std::string& kernel) { return unary(d, kernel, false); }
+  DeviceDataset map_cl(const DeviceDataset& d, const std::string& kernel) {
+    TraceRange trace("ucores.map_cl/" + kernel);
+    return unary(d, kernel, false);
+  }
 
   /// Engine::map_cl_partition (engine.hpp:89-114) over the concatenated
   /// partitions: axpb, psum, pmax, sobel (pi / matmul fail as in the
   /// reference unless a partition holds exactly one element).
   DeviceDataset map_cl_partition(const DeviceDataset& d, const std::string& kernel) {
+    TraceRange trace("ucores.map_cl_partition/" + kernel);
     for (std::size_t p = 0; p < d.parts_.size(); ++p) {
       if (d.parts_[p].sizes.empty()) {
         fail(p, "map_parameters: element kind mismatch, have bytes (empty partition concatenates to an empty "
@@ -330,6 +338,7 @@ class DeviceEngine {
 
   /// Engine::reduce_cl (engine.hpp:121-192): sum2, max2, vectoradd, isum2.
   ucores::Element reduce_cl(const DeviceDataset& d, const std::string& kernel) {
+    TraceRange trace("ucores.reduce_cl/" + kernel);
     const bool i64 = kernel == "isum2";
     if (!i64 && kernel != "sum2" && kernel != "max2" && kernel != "vectoradd") {
       throw ucores::UnknownKernel("no device reduce_cl body for kernel '" + kernel + "'");

@@ -32,6 +32,7 @@
 #include "ucores_b200/cuda_executor.hpp"
 #include "ucores_b200/device_ops.hpp"
 #include "ucores_b200/gpu_context.hpp"
+#include "ucores_b200/trace.hpp"
 
 namespace ucores_b200 {
 
@@ -67,6 +68,7 @@ class GpuClusterDriver : public ucores::ClusterDriver {
 
   std::vector<ucores::TaskResult> run_wave(std::vector<ucores::Task> tasks, int max_retries) override {
     if (tasks.empty()) return {};
+    TraceRange trace("ucores.run_wave");
     // results are filled in place (a wave of the C1 literal form is 2^20
     // tasks: no per-task optional / failure slots)
     Wave w;
@@ -117,6 +119,7 @@ class GpuClusterDriver : public ucores::ClusterDriver {
   void run_batch(const std::vector<ucores::Task>& tasks, const DeviceOp& op, const std::vector<std::size_t>& idx,
                  std::size_t lo, std::size_t hi, std::size_t g, Wave& w) {
     if (lo >= hi) return;
+    TraceRange trace("ucores.batch " + tasks[idx[lo]].kernel_name + " gpu" + std::to_string(g));
     std::vector<const ucores::Task*> batch;
     batch.reserve(hi - lo);
     for (std::size_t k = lo; k < hi; ++k) batch.push_back(&tasks[idx[k]]);

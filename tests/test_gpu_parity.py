@@ -550,3 +550,25 @@ def test_tapered_tail_bitexact():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "5 passed" in r.stdout, r.stdout[-2000:]
 
+
+
+@pytest.mark.parametrize("env", [{}, {"UCG_SOBEL_STATIC": "1"}, {"UCG_SOBEL_ARITH": "half"},
+                                 {"UCG_SOBEL_VARIANT": "0"}, {"UCG_SOBEL_VARIANT": "0", "UCG_SOBEL_ARITH": "half"},
+                                 {"UCG_SOBEL_VARIANT": "2"}], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+def test_sobel_kernel_variants(cuda, env):
+    """Every Sobel kernel (TMA tiles with claimed or round-robin tiles, row
+    streaming, register streaming) in both arithmetic forms (biased integer,
+    fp16-subnormal) is bit-exact against the oracle on random images and on
+    saturating patterns."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent
+    out = subprocess.run([sys.executable, str(here / "sobel_variant_worker.py")], env=dict(os.environ, **env),
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-3000:]
+    rep = json.loads(out.stdout.strip().splitlines()[-1])
+    assert rep["cases"] >= 14 and rep["bad"] == [], rep
