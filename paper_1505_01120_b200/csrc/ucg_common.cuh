@@ -95,11 +95,13 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // The two reduce combines. SUM: IEEE a+b (identity -0.0f, exact for every
 // operand); MAX: std::max(a,b) == (a<b)?b:a (identity -inf as right operand).
 struct OpSum {
+  static constexpr int kId = 0;
   static __device__ __forceinline__ float apply(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float identity() { return -0.0f; }
   static __device__ __forceinline__ float empty() { return 0.0f; }
 };
 struct OpMax {
+  static constexpr int kId = 1;
   static __device__ __forceinline__ float apply(float a, float b) { return (a < b) ? b : a; }
   static __device__ __forceinline__ float identity() { return __int_as_float(0xff800000); }
   static __device__ __forceinline__ float empty() { return __int_as_float(0xff800000); }
@@ -133,8 +135,10 @@ struct ucg_segtab {
   uint32_t* d_item_seg;    // [nitems]
   uint64_t max_items_per_seg;
   int item_log2;           // work-item size (floats) = 2^item_log2, chosen per table
-  uint32_t* d_done;        // [4] pass-1 exit / finisher / item counters (zero between launches)
+  uint32_t* d_done;        // [2][4] pass-1 exit / finisher / item counters per launch parity
+                           // (zero between launches of that parity)
   uint64_t ntaper;         // trailing items the fused map streams as 4 sub-items each (0: none)
+  mutable uint64_t launches = 0;  // pass-1 launches so far: parity selects the counter and scratch half
 };
 
 // Peer-exchange context of a sharded reduce_cl (one process per GPU).
@@ -157,6 +161,14 @@ struct ucg_xchg {
 };
 
 namespace ucg {
+// Floats of scratch one pass-1 launch uses (item roots, then the tapered
+// tail's sub-roots), rounded to 16 bytes; the caller's scratch holds two such
+// halves, used by alternate launches so a step's stream can overlap the
+// previous step's partition trees (ucg_reduce.cu segment_reduce).
+inline uint64_t scratch_half(const ucg_segtab* t) {
+  const uint64_t n = t->ntaper ? ((t->nitems + 4) & ~uint64_t(3)) + 4 * t->ntaper : t->nitems + 1;
+  return (n + 3) & ~uint64_t(3);
+}
 // Work item = one aligned block of 2^item_log2 floats of one segment (the
 // last item of a segment may be partial). The size is picked per segment
 // table in [2^11, 2^14] so the last wave of warps is nearly full.

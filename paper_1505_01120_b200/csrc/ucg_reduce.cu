@@ -24,7 +24,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -563,6 +565,10 @@ struct Pass1Args {
   float* partial;
   int finish;
   int dynamic;  // claim items from the counter fin.done[2] instead of grid-stride
+  // 1: the previous kernel in the stream is the same step on the same table
+  // and buffers (segment_reduce checks): stream first, wait for it only
+  // before the partition trees, so this step's stream overlaps its tail
+  int early;
   FinishArgs fin;
 };
 
@@ -572,8 +578,17 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   // may be resident before the previous step's grid has finished; wait for it
   // (its y, partials and counter reset) before touching memory, and let the
   // next step's grid launch now. Both are no-ops without the launch attribute.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  //
+  // Early mode (repeated steps, see Pass1Args::early): the stream only reads
+  // x and writes y (the same values), item roots and claims of this launch's
+  // parity half, so it starts at once; the finishers wait for the previous
+  // step (whose trees may still run) before its counters, partition values
+  // and exchange, and only then let the next step launch — which therefore
+  // never overlaps a step of its own parity.
+  if (!p.early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarps;
@@ -629,6 +644,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   }
   __syncthreads();
   if (ticket + F < G) return;
+  if (p.early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     // every CTA is resident (cooperative launch), so the others finish their
     // stream; a wait of kPeerWaitNs cannot happen — trap rather than reduce
@@ -897,7 +916,10 @@ cudaError_t launch_pass1(const Pass1Args& args, const ucg_segtab* t, cudaStream_
   // validates), and the next step's CTAs park in griddepcontrol.wait only in
   // slots this grid has left, so every CTA of this grid is already resident.
   static const bool pdl_multi = getenv("UCG_PDL_MULTI") != nullptr;
-  if (args.finish && args.fin.finishers != 1 && !(pdl_multi && !no_pdl)) {
+  // An early-mode launch is a PDL launch (its CTAs become resident as the
+  // previous step's CTAs leave; its finishers wait only for CTAs of its own
+  // grid, which all get slots once the previous finishers exit).
+  if (args.finish && args.fin.finishers != 1 && !args.early && !(pdl_multi && !no_pdl)) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.numAttrs = 1;
@@ -942,6 +964,36 @@ inline bool separate_finish() {
   return v;
 }
 
+// Early mode is safe when the kernel just before this one in the stream is
+// the same fused step (same table, buffers, map and op): then the only early
+// overlap is that step's partition trees, and this step's stream touches
+// nothing they read. Any other pass-1 launch on the stream breaks the chain;
+// other kernels and copies never trigger their dependents early, so a
+// programmatic launch after them starts only when they have completed.
+// UCG_NO_EARLY (A/B): never.
+inline bool repeat_of_last_pass1(cudaStream_t st, const ucg_segtab* t, const float* x, const float* y, float a,
+                                 float b, const float* out, const float* result, const ucg_xchg* xg, int op) {
+  struct Key {
+    const void* t;
+    const void *x, *y, *out, *result, *xg;
+    float a, b;
+    int op;
+    bool operator==(const Key& o) const {
+      return t == o.t && x == o.x && y == o.y && out == o.out && result == o.result && xg == o.xg &&
+             std::memcmp(&a, &o.a, 4) == 0 && std::memcmp(&b, &o.b, 4) == 0 && op == o.op;
+    }
+  };
+  static const bool off = getenv("UCG_NO_EARLY") != nullptr || getenv("UCG_NO_PDL") != nullptr;
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, Key> last;
+  const Key k{t, x, y, out, result, xg, a, b, op};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = last.find(st);
+  const bool same = it != last.end() && it->second == k;
+  last[st] = k;
+  return same && !off;
+}
+
 // Pass 1 with the partition trees and reduce_cl stage 2 folded into its tail
 // (one launch per step); a table without work items launches the stand-alone
 // finish kernel instead.
@@ -954,7 +1006,12 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     return fail(UCG_ERR_ARG, "segment table was created on device " + std::to_string(t->device) +
                                  ", current device is " + std::to_string(dev));
   }
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, t->d_done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0, 0};
+  // launch parity: alternate launches use alternate counter sets and scratch
+  // halves, so a step may stream while the previous one finishes
+  const uint64_t par = t->launches++ & 1;
+  scratch += par * scratch_half(t);
+  uint32_t* done = t->d_done + 4 * par;
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -992,7 +1049,8 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
   }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
-                   a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, f};
+                   a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, 0, f};
+    args.early = fused_finish && repeat_of_last_pass1(st, t, x, y, a, b, out, result, xg, Op::kId) ? 1 : 0;
     const cudaError_t e = y ? dispatch_pass1<Op, true>(args, t, st) : dispatch_pass1<Op, false>(args, t, st);
     UCG_CUDA(e);
     UCG_LAUNCHED();

@@ -388,8 +388,8 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if ((e = cudaMalloc(&t->d_len, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_first_item, (nseg + 1) * 8)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMalloc(&t->d_done, 16)) != cudaSuccess) return cleanup(e, "cudaMalloc");
-  if ((e = cudaMemset(t->d_done, 0, 16)) != cudaSuccess) return cleanup(e, "cudaMemset");
+  if ((e = cudaMalloc(&t->d_done, 32)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMemset(t->d_done, 0, 32)) != cudaSuccess) return cleanup(e, "cudaMemset");
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
@@ -533,7 +533,7 @@ int ucg_xchg_destroy(ucg_xchg* x) {
 
 int ucg_segtab_scratch_floats(const ucg_segtab* t, uint64_t* n_out) {
   if (!t || !n_out) return fail(UCG_ERR_ARG, "null argument");
-  *n_out = t->ntaper ? ((t->nitems + 4) & ~uint64_t(3)) + 4 * t->ntaper : t->nitems + 1;
+  *n_out = 2 * ucg::scratch_half(t);  // one half per launch parity (consecutive steps overlap)
   return UCG_OK;
 }
 

@@ -205,16 +205,16 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
 // O = 4k+1, 4k+3; Le / Ro = the left neighbours of the even pixels and the
 // right neighbours of the odd ones).
 //
-// kHalf (UCG_SOBEL_ARITH=half): each 16-bit half holding a byte p is read as the fp16
+// kHalf (default): each 16-bit half holding a byte p is read as the fp16
 // SUBNORMAL p * 2^-24. Every intermediate (dh, sh, Gx, Gy, |Gx|+|Gy|) is an
 // integer multiple of 2^-24 of magnitude <= 2040 < 2048, so HADD2/HFMA2 are
 // exact; |.| is a free operand modifier of HADD2, the clamp is one HMNMX2 and
 // min(|Gx|+|Gy|, 255) * 2^-24 has the output byte as its low byte. The work
 // lands on the FMA pipe (HADD2/HFMA2), leaving the ALU pipe the byte permutes.
-// Integer form (default): biased u16x2 lanes, IMAD on the FMA pipe and
-// VIMNMX/IADD3 on the ALU pipe. The fp16 form moves the arithmetic off the
-// ALU pipe onto the fp16 pipe, which runs at the same half rate; it measured
-// no faster.
+// Integer form (UCG_SOBEL_ARITH=int, round 1): biased u16x2 lanes, IMAD on
+// the FMA pipe and VIMNMX/IADD3 on the ALU pipe. The fp16 pipe runs at the
+// same half rate as the ALU pipe, so the fp16 form issues no faster; it wins
+// at the power cap, where its cheaper adders keep the clocks up.
 __device__ __forceinline__ __half2 h2_of(uint32_t u) {
   __half2 h;
   memcpy(&h, &u, 4);
@@ -675,12 +675,14 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
     const char* e = getenv("UCG_SOBEL_VARIANT");
     return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 1);
   }();
-  // UCG_SOBEL_ARITH=half (A/B runs): the fp16-subnormal arithmetic instead of
-  // the integer form (measured: 98.8 vs 100.7 us alone under ncu, but 110 vs
-  // 99 us back to back — the fp16 pipe is half rate like the ALU pipe)
+  // UCG_SOBEL_ARITH=int (A/B runs): the integer arithmetic instead of the
+  // fp16-subnormal form. Measured at steady state (the GPU at its power cap):
+  // 93.7 vs 103.7 us over 2000 back-to-back launches, 101 vs 110 us in the
+  // bench line — the fp16 adds draw less power than IMAD-as-adder, so the
+  // clocks stay higher; alone under ncu the two are equal (98.8 vs 100.7 us)
   static const bool half_arith = [] {
     const char* e = getenv("UCG_SOBEL_ARITH");
-    return e && strcmp(e, "half") == 0;
+    return !(e && strcmp(e, "int") == 0);
   }();
   bool rows_ok = vec && variant == 0 && width < (1ull << 31);
   for (uint64_t i = 0; i < nbands && rows_ok; ++i) rows_ok = in_off[i] % width == 0;

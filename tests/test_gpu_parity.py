@@ -572,3 +572,54 @@ def test_sobel_kernel_variants(cuda, env):
     assert out.returncode == 0, out.stderr[-3000:]
     rep = json.loads(out.stdout.strip().splitlines()[-1])
     assert rep["cases"] >= 14 and rep["bad"] == [], rep
+
+
+# ---- consecutive steps (early-stream mode) --------------------------------------------
+
+@pytest.mark.parametrize("lens", [[1 << 20] * 4, [3 << 22, 77777, 1, 1 << 21, 5 << 20]])
+@pytest.mark.parametrize("op", ["sum", "max"])
+def test_consecutive_steps_early_mode(cuda, lens, op):
+    """Back-to-back steps on one table overlap (each step's stream runs while
+    the previous step's partition trees finish, on alternate counter and
+    scratch halves): after odd and even numbers of chained steps the partials
+    and result are bit-exact; an input rewritten by another kernel between
+    steps is seen by the next step; a table reducing another table's output
+    right after it reads that output complete."""
+    from paper_1505_01120_b200 import ops
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    def want(xs, a, b):
+        p = [O.tree_reduce(O.map_affine(x, a, b), op) for x in xs]
+        return np.array(p, np.float32), O.tree_reduce(np.array(p, np.float32), op)
+
+    pipe = MapReducePipeline(lens, op=op, plant_max=False)
+    xs = [O.fill_uniform(1000 + k, n) for k, n in enumerate(lens)]
+    wp, wr = want(xs, 2.0, 1.0)
+    for chain in (7, 4):
+        for _ in range(chain):
+            r = pipe.step()
+        torch.cuda.synchronize()
+        assert np.array_equal(_bits(pipe.partials), wp.view(np.uint32)), chain
+        assert O.f32_bits(r.cpu().numpy()[0]) == O.f32_bits(wr), chain
+    # a torch kernel rewrites x between two chained steps
+    pipe.step()
+    pipe.x.mul_(0.5)
+    r = pipe.step()
+    pipe.step()
+    torch.cuda.synchronize()
+    wp2, wr2 = want([x * np.float32(0.5) for x in xs], 2.0, 1.0)
+    assert np.array_equal(_bits(pipe.partials), wp2.view(np.uint32))
+    assert O.f32_bits(r.cpu().numpy()[0]) == O.f32_bits(wr2)
+    # a second table reduces the first's y right after the first's steps
+    pipe2 = MapReducePipeline(lens, op=op, plant_max=False)
+    for _ in range(3):
+        pipe.step()
+    ops.segment_reduce_cl(pipe.y, None, pipe2.segtab, 1.0, 0.0, op, pipe2.scratch, pipe2.partials, None,
+                          pipe2.result)
+    torch.cuda.synchronize()
+    ys = [pipe.y[b:b + n].cpu().numpy() for b, n in zip(pipe.layout.begins, lens)]
+    wp3 = np.array([O.tree_reduce(y, op) for y in ys], np.float32)
+    assert np.array_equal(_bits(pipe2.partials), wp3.view(np.uint32))
+    assert O.f32_bits(pipe2.result.cpu().numpy()[0]) == O.f32_bits(O.tree_reduce(wp3, op))
+    pipe.close()
+    pipe2.close()
