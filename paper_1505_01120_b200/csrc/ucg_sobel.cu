@@ -205,16 +205,18 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
 // O = 4k+1, 4k+3; Le / Ro = the left neighbours of the even pixels and the
 // right neighbours of the odd ones).
 //
-// kHalf (default): each 16-bit half holding a byte p is read as the fp16
-// SUBNORMAL p * 2^-24. Every intermediate (dh, sh, Gx, Gy, |Gx|+|Gy|) is an
-// integer multiple of 2^-24 of magnitude <= 2040 < 2048, so HADD2/HFMA2 are
-// exact; |.| is a free operand modifier of HADD2, the clamp is one HMNMX2 and
-// min(|Gx|+|Gy|, 255) * 2^-24 has the output byte as its low byte. The work
-// lands on the FMA pipe (HADD2/HFMA2), leaving the ALU pipe the byte permutes.
-// Integer form (UCG_SOBEL_ARITH=int, round 1): biased u16x2 lanes, IMAD on
-// the FMA pipe and VIMNMX/IADD3 on the ALU pipe. The fp16 pipe runs at the
-// same half rate as the ALU pipe, so the fp16 form issues no faster; it wins
-// at the power cap, where its cheaper adders keep the clocks up.
+// fp16 forms (kArith 1-3; 2 is the default): each 16-bit half holding a
+// byte p is read as the fp16 SUBNORMAL p * 2^-24, and more generally any
+// integer v in [0, 2048) stored in a half IS the fp16 value v * 2^-24. Every
+// intermediate (dh, sh, Gx, Gy, |Gx|+|Gy|) is an integer multiple of 2^-24 of
+// magnitude <= 2040, so HADD2/HFMA2 are exact; |.| is a free operand
+// modifier of HADD2, the clamp is one HMNMX2, and min(|Gx|+|Gy|, 255) * 2^-24
+// has the output byte as its low byte. The non-negative sh terms can equally
+// be added as plain u16x2 integers on the ALU pipe (forms 2 and 3), which
+// balances the ALU and fp16 pipes — both half rate.
+// Integer form (kArith 0, round 1): biased u16x2 lanes, IMAD on the FMA pipe
+// and VIMNMX/IADD3 on the ALU pipe; slowest at the power cap (IMAD as an
+// adder costs more power than HADD2, so the clocks drop further).
 __device__ __forceinline__ __half2 h2_of(uint32_t u) {
   __half2 h;
   memcpy(&h, &u, 4);
@@ -228,16 +230,21 @@ __device__ __forceinline__ uint32_t u_of(__half2 h) {
 
 // row terms of one 4-pixel word: dh = R - L, sh = L + 2C + R for the even and
 // the odd plane (integer form: unbiased, exact mod 2^32 on the packed word)
-template <bool kHalf>
+template <int kArith>
 __device__ __forceinline__ void word_terms(uint32_t E, uint32_t O, uint32_t Le, uint32_t Ro, uint32_t one,
                                            uint32_t two, uint32_t m1, uint32_t& dhe, uint32_t& dho, uint32_t& she,
                                            uint32_t& sho) {
-  if constexpr (kHalf) {
+  if constexpr (kArith != 0) {
     const __half2 e = h2_of(E), o = h2_of(O), l = h2_of(Le), r = h2_of(Ro), k2 = __float2half2_rn(2.f);
     dhe = u_of(__hsub2(o, l));
     dho = u_of(__hsub2(r, e));
-    she = u_of(__hfma2(e, k2, __hadd2(l, o)));
-    sho = u_of(__hfma2(o, k2, __hadd2(e, r)));
+    // sh is non-negative and < 2048: its integer bits ARE the fp16 value
+    // sh * 2^-24, so arithmetic forms 2 / 3 add it on the ALU pipe instead
+    // (plain u16x2 adds, no carries) to balance the two half-rate pipes
+    if constexpr (kArith >= 2) she = Le + O + E + E;
+    else she = u_of(__hfma2(e, k2, __hadd2(l, o)));
+    if constexpr (kArith == 3) sho = E + Ro + O + O;
+    else sho = u_of(__hfma2(o, k2, __hadd2(e, r)));
   } else {
     dhe = mad_u32(Le, m1, O);
     dho = mad_u32(E, m1, Ro);
@@ -248,10 +255,10 @@ __device__ __forceinline__ void word_terms(uint32_t E, uint32_t O, uint32_t Le, 
 
 // one packed output pair from input rows (a, b, c) = (r, r+1, r+2); the
 // output bytes are the low bytes of the two halves
-template <bool kHalf>
+template <int kArith>
 __device__ __forceinline__ uint32_t out_pair(uint32_t adh, uint32_t bdh, uint32_t cdh, uint32_t ash, uint32_t csh,
                                              uint32_t two, uint32_t m1) {
-  if constexpr (kHalf) {
+  if constexpr (kArith != 0) {
     const __half2 gx = __hfma2(h2_of(bdh), __float2half2_rn(2.f), __hadd2(h2_of(adh), h2_of(cdh)));
     const __half2 gy = __hsub2(h2_of(csh), h2_of(ash));
     return u_of(__hmin2(__hadd2(__habs2(gx), __habs2(gy)), h2_of(0x00FF00FFu)));
@@ -316,7 +323,7 @@ __device__ __forceinline__ void issue_tile(const SobelMaps* maps, const SobelTil
         : "memory");
 }
 
-template <bool kHalf>
+template <int kArith>
 __global__ void __launch_bounds__(kTmaThreads)
     k_sobel_tma(const __grid_constant__ SobelMaps maps, uint8_t* __restrict__ out, const __grid_constant__ SobelTiles p,
                 uint64_t width, unsigned long long* __restrict__ ctr) {
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         // left of the even pixels (p[4k-1], p[4k+1]); right of the odd ones (p[4k+2], p[4k+4])
         const uint32_t Le = k ? __byte_perm(O[k - 1], O[k], 0x5432) : __byte_perm(pw, O[0], 0x5453);
         const uint32_t Ro = k < 3 ? __byte_perm(E[k], E[k + 1], 0x5432) : __byte_perm(E[3], nw, 0x1432);
-        word_terms<kHalf>(E[k], O[k], Le, Ro, one, two, m1, tr.dh[2 * k], tr.dh[2 * k + 1], tr.sh[2 * k],
+        word_terms<kArith>(E[k], O[k], Le, Ro, one, two, m1, tr.dh[2 * k], tr.dh[2 * k + 1], tr.sh[2 * k],
                           tr.sh[2 * k + 1]);
       }
     };
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       if (uint32_t(rg * 8 + r) >= valid_rows || col >= width) return;
       uint32_t o[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = out_pair<kHalf>(a.dh[i], bb.dh[i], c.dh[i], a.sh[i], c.sh[i], two, m1);
+      for (int i = 0; i < 8; ++i) o[i] = out_pair<kArith>(a.dh[i], bb.dh[i], c.dh[i], a.sh[i], c.sh[i], two, m1);
       // interleave the planes back: bytes (even lo, odd lo, even hi, odd hi)
       const uint32_t q0 = __byte_perm(o[0], o[1], 0x6240), q1 = __byte_perm(o[2], o[3], 0x6240);
       const uint32_t q2 = __byte_perm(o[4], o[5], 0x6240), q3 = __byte_perm(o[6], o[7], 0x6240);
@@ -486,7 +493,7 @@ struct SobelRows {
   uint32_t mul[3];                    // {1, 2, 0xFFFFFFFF}, opaque to the compiler
 };
 
-template <int kMinBlocks, int kSlots, int kCols, bool kHalf>
+template <int kMinBlocks, int kSlots, int kCols, int kArith>
 __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
     k_sobel_rows(const __grid_constant__ CUtensorMap rows3, uint8_t* __restrict__ out,
                  const __grid_constant__ SobelRows p, uint64_t width) {
@@ -569,14 +576,14 @@ __global__ void __launch_bounds__(kRowThreads, kMinBlocks)
       for (int kk = 0; kk < kW; ++kk) {
         const uint32_t Le = kk ? __byte_perm(O[kk - 1], O[kk], 0x5432) : __byte_perm(pw, O[0], 0x5453);
         const uint32_t Ro = kk < kW - 1 ? __byte_perm(E[kk], E[kk + 1], 0x5432) : __byte_perm(E[kW - 1], nw2, 0x1432);
-        word_terms<kHalf>(E[kk], O[kk], Le, Ro, one, two, m1, tr.dh[2 * kk], tr.dh[2 * kk + 1], tr.sh[2 * kk],
+        word_terms<kArith>(E[kk], O[kk], Le, Ro, one, two, m1, tr.dh[2 * kk], tr.dh[2 * kk + 1], tr.sh[2 * kk],
                           tr.sh[2 * kk + 1]);
       }
     };
     auto emit = [&](uint32_t r, const RowTermsW<kW>& a, const RowTermsW<kW>& bb, const RowTermsW<kW>& c) {
       uint32_t o[2 * kW];
 #pragma unroll
-      for (int i = 0; i < 2 * kW; ++i) o[i] = out_pair<kHalf>(a.dh[i], bb.dh[i], c.dh[i], a.sh[i], c.sh[i], two, m1);
+      for (int i = 0; i < 2 * kW; ++i) o[i] = out_pair<kArith>(a.dh[i], bb.dh[i], c.dh[i], a.sh[i], c.sh[i], two, m1);
       if (active) {
         uint32_t x[kW];
 #pragma unroll
@@ -675,14 +682,22 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
     const char* e = getenv("UCG_SOBEL_VARIANT");
     return e ? atoi(e) : (getenv("UCG_SOBEL_NO_TMA") ? 2 : 1);
   }();
-  // UCG_SOBEL_ARITH=int (A/B runs): the integer arithmetic instead of the
-  // fp16-subnormal form. Measured at steady state (the GPU at its power cap):
-  // 93.7 vs 103.7 us over 2000 back-to-back launches, 101 vs 110 us in the
-  // bench line — the fp16 adds draw less power than IMAD-as-adder, so the
-  // clocks stay higher; alone under ncu the two are equal (98.8 vs 100.7 us)
-  static const bool half_arith = [] {
+  // Arithmetic form (UCG_SOBEL_ARITH for A/B runs): mix (default) = fp16-
+  // subnormal with the even plane's sh terms added on the ALU pipe; half =
+  // all fp16; mix2 = both planes' sh on the ALU pipe; int = the round-1
+  // biased-integer form. Same box, claimed tiles (profiles/r02/sobel_claim/):
+  // bench line (1 s soak, power-capped ~1.7 GHz) mix 95.5-96.8 us, half
+  // 99.2, mix2 97.6, int 107.9; 2000 back-to-back launches mix 90.2-91.1,
+  // half 91.9-92.7, int 102.1; alone under ncu mix 86.7, half 89.2. The fp16
+  // adds cost less power than IMAD-as-adder (clocks stay higher at the cap)
+  // and balance the FMA and ALU pipes, which both run at half rate.
+  static const int arith = [] {
     const char* e = getenv("UCG_SOBEL_ARITH");
-    return !(e && strcmp(e, "int") == 0);
+    if (!e) return 2;
+    if (strcmp(e, "int") == 0) return 0;
+    if (strcmp(e, "half") == 0) return 1;
+    if (strcmp(e, "mix2") == 0) return 3;
+    return 2;
   }();
   bool rows_ok = vec && variant == 0 && width < (1ull << 31);
   for (uint64_t i = 0; i < nbands && rows_ok; ++i) rows_ok = in_off[i] % width == 0;
@@ -697,10 +712,12 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       const char* e = getenv("UCG_SOBEL_SLOTS");
       return e && atoi(e) == 6 ? 6 : 4;
     }();
-    auto kern = half_arith ? (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, true> : k_sobel_rows<5, 4, 16, true>)
-                                         : (slots == 6 ? k_sobel_rows<8, 6, 8, true> : k_sobel_rows<8, 4, 8, true>))
-                           : (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, false> : k_sobel_rows<5, 4, 16, false>)
-                                         : (slots == 6 ? k_sobel_rows<8, 6, 8, false> : k_sobel_rows<8, 4, 8, false>));
+    // row streaming (A/B only): 16 or 8 columns per lane, integer or fp16 form
+    const bool half = arith != 0;
+    auto kern = half ? (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, 1> : k_sobel_rows<5, 4, 16, 1>)
+                                   : (slots == 6 ? k_sobel_rows<8, 6, 8, 1> : k_sobel_rows<8, 4, 8, 1>))
+                     : (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, 0> : k_sobel_rows<5, 4, 16, 0>)
+                                   : (slots == 6 ? k_sobel_rows<8, 6, 8, 0> : k_sobel_rows<8, 4, 8, 0>));
     const uint32_t smem = cols == 16 ? (slots == 6 ? sobel_rows_smem<6, 16>() : sobel_rows_smem<4, 16>())
                                      : (slots == 6 ? sobel_rows_smem<6, 8>() : sobel_rows_smem<4, 8>());
     const uint32_t seg_cols = 32u * uint32_t(cols);
@@ -778,7 +795,7 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) return fail(UCG_ERR_CUDA, "sobel tensor map encode failed");
-    auto tkern = half_arith ? k_sobel_tma<true> : k_sobel_tma<false>;
+    auto tkern = arith == 0 ? k_sobel_tma<0> : arith == 2 ? k_sobel_tma<2> : arith == 3 ? k_sobel_tma<3> : k_sobel_tma<1>;
     static std::atomic<uint64_t> attr{0};
     if (first_on_device(attr))
       UCG_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * kBufBytes + 128)));

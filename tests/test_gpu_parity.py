@@ -552,13 +552,14 @@ def test_tapered_tail_bitexact():
 
 
 
-@pytest.mark.parametrize("env", [{}, {"UCG_SOBEL_STATIC": "1"}, {"UCG_SOBEL_ARITH": "half"},
-                                 {"UCG_SOBEL_VARIANT": "0"}, {"UCG_SOBEL_VARIANT": "0", "UCG_SOBEL_ARITH": "half"},
+@pytest.mark.parametrize("env", [{}, {"UCG_SOBEL_STATIC": "1"}, {"UCG_SOBEL_ARITH": "int"},
+                                 {"UCG_SOBEL_ARITH": "half"}, {"UCG_SOBEL_ARITH": "mix2"},
+                                 {"UCG_SOBEL_VARIANT": "0"}, {"UCG_SOBEL_VARIANT": "0", "UCG_SOBEL_ARITH": "int"},
                                  {"UCG_SOBEL_VARIANT": "2"}], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_sobel_kernel_variants(cuda, env):
     """Every Sobel kernel (TMA tiles with claimed or round-robin tiles, row
-    streaming, register streaming) in both arithmetic forms (biased integer,
-    fp16-subnormal) is bit-exact against the oracle on random images and on
+    streaming, register streaming) in every arithmetic form (fp16-subnormal,
+    biased integer, the mixed forms) is bit-exact against the oracle on random images and on
     saturating patterns."""
     import json
     import os
