@@ -129,7 +129,11 @@ int ucg_fill_bytes_u8(uint8_t* out, uint64_t n, uint64_t seed, uint64_t first, v
 typedef struct ucg_segtab ucg_segtab;
 int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg, ucg_segtab** out);
 int ucg_segtab_destroy(ucg_segtab* t);
-/* scratch floats the segment reductions need for a table (work-item partials) */
+/* scratch floats the segment reductions need for a table: two halves of
+ * work-item partials, used by alternate launches on the table, so a repeated
+ * step (same table, buffers, map and op as the kernel before it in the
+ * stream) streams while the previous step's partition trees finish. The
+ * scratch must stay the same buffer across such repeated steps. */
 int ucg_segtab_scratch_floats(const ucg_segtab* t, uint64_t* n_out);
 
 /* ------------------------------------------------------------------------ */
