@@ -138,6 +138,7 @@ struct ucg_segtab {
   uint32_t* d_done;        // [2][4] pass-1 exit / finisher / item counters per launch parity
                            // (zero between launches of that parity)
   uint64_t ntaper;         // trailing items the fused map streams as 4 sub-items each (0: none)
+  unsigned long long* d_gen;  // [2][2] per parity: start tickets, completed fused grids (never reset)
   mutable uint64_t launches = 0;  // pass-1 launches so far: parity selects the counter and scratch half
 };
 

@@ -279,6 +279,7 @@ struct FinishArgs {
   uint64_t nseg;
   float* out;                 // this rank's per-segment (partition) values
   uint32_t* done;             // [3] pass-1 exit / finisher / item counters, zero between launches
+  unsigned long long* gen;    // [2] this parity's {start tickets, completed grids} (fused launches)
   float* result;              // reduce_cl result (every rank gets it), or null
   // sharded exchange (world > 1): region r = rank r's IPC-mapped buffer
   int world, rank;
@@ -312,6 +313,11 @@ __device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
 __device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -426,6 +432,15 @@ __device__ __noinline__ void peer_timeout(const FinishArgs& p) {
   }
 }
 
+// This grid is done with its parity's counters and item roots (every tree
+// is built and the counters are zero again): count it as completed, so the
+// next grid of this parity may start streaming (see k_segment_pass1).
+__device__ __forceinline__ void release_parity(const FinishArgs& p) {
+  if (!p.gen) return;
+  __threadfence();
+  atomicAdd(p.gen + 1, 1ull);
+}
+
 // Called by all F finisher CTAs after their segments are written. The last
 // one to arrive resets the counters and runs reduce_cl stage 2: on one GPU
 // directly over the partition values; sharded, it first stores this rank's
@@ -445,6 +460,7 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
       p.done[0] = 0;
       p.done[1] = 0;
       p.done[2] = 0;
+      release_parity(p);
     }
   } else {
     if (tid == 0) {
@@ -457,6 +473,7 @@ __device__ void stage2(const FinishArgs& p, uint32_t F, TreeSmem& sm) {
       p.done[0] = 0;
       p.done[1] = 0;
       p.done[2] = 0;
+      release_parity(p);
     }
     __threadfence();
   }
@@ -569,6 +586,7 @@ struct Pass1Args {
   // and buffers (segment_reduce checks): stream first, wait for it only
   // before the partition trees, so this step's stream overlaps its tail
   int early;
+  int early_top;  // early mode, next step triggered at the top (A/B: UCG_EARLY_TOP)
   FinishArgs fin;
 };
 
@@ -585,9 +603,32 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   // step (whose trees may still run) before its counters, partition values
   // and exchange, and only then let the next step launch — which therefore
   // never overlaps a step of its own parity.
+  //
+  // Early mode with the trigger at the top (UCG_EARLY_TOP): the next step may
+  // launch at once and its CTAs take the slots this grid's CTAs leave as
+  // they finish the stream (the ragged end of the stream overlaps the next
+  // step). A grid then may start while the previous grid of its parity is
+  // still running, so each CTA takes a start ticket of its parity — ticket
+  // / G is the number of earlier fused grids of that parity — and waits
+  // until that many have released the parity (release_parity).
   if (!p.early) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (p.fin.gen && p.finish && threadIdx.x == 0) atomicAdd(p.fin.gen, 1ull);  // keep the ticket count
+  } else if (p.early_top) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) {
+      const unsigned long long g = atomicAdd(p.fin.gen, 1ull) / gridDim.x;
+      const uint64_t t0 = global_ns();
+      uint32_t spins = 0;
+      while (ld_acquire_gpu_u64(p.fin.gen + 1) < g) {
+        __nanosleep(64);
+        if ((++spins & 1023) == 0 && global_ns() - t0 > kPeerWaitNs) __trap();
+      }
+    }
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    atomicAdd(p.fin.gen, 1ull);  // keep the ticket count
   }
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
@@ -646,7 +687,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   if (ticket + F < G) return;
   if (p.early) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!p.early_top) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   if (threadIdx.x == 0) {
     // every CTA is resident (cooperative launch), so the others finish their
@@ -1011,7 +1052,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
   const uint64_t par = t->launches++ & 1;
   scratch += par * scratch_half(t);
   uint32_t* done = t->d_done + 4 * par;
-  FinishArgs f{scratch, t->d_first_item, t->nseg, out, done, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0, 0};
+  FinishArgs f{scratch, t->d_first_item, t->nseg, out, done, t->d_gen + 2 * par, result, 1, 0, 0, t->nseg, nullptr, 0, nullptr, nullptr, 0, 0, 0, 0};
   if (xg) {
     f.world = xg->world;
     f.rank = xg->rank;
@@ -1049,8 +1090,14 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
   }
   if (t->nitems) {
     Pass1Args args{x, y, t->d_begin, t->d_len, t->d_first_item, t->d_item_seg, t->nitems, t->item_log2,
-                   a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, 0, f};
-    args.early = fused_finish && repeat_of_last_pass1(st, t, x, y, a, b, out, result, xg, Op::kId) ? 1 : 0;
+                   a, b, scratch, fused_finish ? 1 : 0, dynamic_items() ? 1 : 0, 0, 0, f};
+    // every pass-1 launch updates the tracker (a different launch in between
+    // breaks the chain); only a fused one may run early
+    const bool repeat = repeat_of_last_pass1(st, t, x, y, a, b, out, result, xg, Op::kId);
+    args.early = fused_finish && repeat ? 1 : 0;
+    static const bool early_top = getenv("UCG_EARLY_TOP") != nullptr;
+    args.early_top = args.early && early_top ? 1 : 0;
+    if (!fused_finish) args.fin.gen = nullptr;  // only fused launches count in the parity tickets
     const cudaError_t e = y ? dispatch_pass1<Op, true>(args, t, st) : dispatch_pass1<Op, false>(args, t, st);
     UCG_CUDA(e);
     UCG_LAUNCHED();
@@ -1215,7 +1262,7 @@ int ucg_reduce_cl_xchg_f32(float* partials, uint64_t nloc, int op, ucg_xchg* xch
     std::lock_guard<std::mutex> lk(mu);
     if (!scratch_done[dev]) UCG_CUDA(cudaMalloc(&scratch_done[dev], 3 * sizeof(unsigned int)));
   }
-  FinishArgs f{nullptr, nullptr, nloc, partials, scratch_done[dev], result, xchg->world, xchg->rank,
+  FinishArgs f{nullptr, nullptr, nloc, partials, scratch_done[dev], nullptr, result, xchg->world, xchg->rank,
                xchg->part_offset, xchg->p_total, xchg->d_peers, xchg->flags_offset, xchg->d_epoch, xchg->d_err, 0, 1,
                getenv("UCG_XCHG_FLAGS") ? 1 : 0, 0};
   cudaStream_t st = as_stream(stream);

@@ -380,6 +380,7 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
     cudaFree(t->d_first_item);
     cudaFree(t->d_item_seg);
     cudaFree(t->d_done);
+    cudaFree(t->d_gen);
     delete t;
     return cuda_fail(e, what);
   };
@@ -390,6 +391,8 @@ int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg,
   if ((e = cudaMalloc(&t->d_item_seg, (nitems + 1) * 4)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMalloc(&t->d_done, 32)) != cudaSuccess) return cleanup(e, "cudaMalloc");
   if ((e = cudaMemset(t->d_done, 0, 32)) != cudaSuccess) return cleanup(e, "cudaMemset");
+  if ((e = cudaMalloc(&t->d_gen, 32)) != cudaSuccess) return cleanup(e, "cudaMalloc");
+  if ((e = cudaMemset(t->d_gen, 0, 32)) != cudaSuccess) return cleanup(e, "cudaMemset");
   if (nseg) {
     if ((e = cudaMemcpy(t->d_begin, begin, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
     if ((e = cudaMemcpy(t->d_len, len, nseg * 8, cudaMemcpyHostToDevice)) != cudaSuccess) return cleanup(e, "cudaMemcpy");
@@ -411,6 +414,7 @@ int ucg_segtab_destroy(ucg_segtab* t) {
   cudaFree(t->d_first_item);
   cudaFree(t->d_item_seg);
   cudaFree(t->d_done);
+  cudaFree(t->d_gen);
   if (cur >= 0 && cur != t->device) cudaSetDevice(cur);
   delete t;
   return UCG_OK;
