@@ -611,14 +611,24 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
   // still running, so each CTA takes a start ticket of its parity — ticket
   // / G is the number of earlier fused grids of that parity — and waits
   // until that many have released the parity (release_parity).
+  //
+  // The ticket is taken BEFORE this CTA triggers its dependents: a grid of
+  // the same parity two launches later exists only after every CTA of this
+  // one has triggered, so tickets of different grids never interleave and
+  // ticket / G is exact (a late CTA of this grid must not draw a ticket
+  // after the next same-parity grid, or it would wait for its own grid).
+  __shared__ unsigned long long start_ticket;
+  if (p.fin.gen && p.finish) {
+    if (threadIdx.x == 0) start_ticket = atomicAdd(p.fin.gen, 1ull);
+    __syncthreads();
+  }
   if (!p.early) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (p.fin.gen && p.finish && threadIdx.x == 0) atomicAdd(p.fin.gen, 1ull);  // keep the ticket count
   } else if (p.early_top) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
-      const unsigned long long g = atomicAdd(p.fin.gen, 1ull) / gridDim.x;
+      const unsigned long long g = start_ticket / gridDim.x;
       const uint64_t t0 = global_ns();
       uint32_t spins = 0;
       while (ld_acquire_gpu_u64(p.fin.gen + 1) < g) {
@@ -627,8 +637,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks) k_segment_pass1(const
       }
     }
     __syncthreads();
-  } else if (threadIdx.x == 0) {
-    atomicAdd(p.fin.gen, 1ull);  // keep the ticket count
   }
   const int lane = threadIdx.x & 31;
   const uint64_t warp = uint64_t(blockIdx.x) * kWarps + (threadIdx.x >> 5);
@@ -1073,6 +1081,7 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     f.ntaper = t->ntaper;
   }
   const bool fused_finish = t->nitems && !separate_finish();
+  if (!fused_finish) f.gen = nullptr;  // only fused launches take parity tickets and release
   // many partitions of few items: a warp per partition tree (the fused tail
   // has only min(G, P) finisher CTAs; G = 2 CTAs per SM)
   f.warp_mode = fused_finish && t->nseg > uint64_t(sm_count()) * 4 &&
@@ -1100,7 +1109,6 @@ int segment_reduce(const float* x, float* y, const ucg_segtab* t, float a, float
     // (A/B): only after this step's stream and the previous step's completion
     static const bool early_top = getenv("UCG_EARLY_LATE_TRIGGER") == nullptr;
     args.early_top = args.early && early_top ? 1 : 0;
-    if (!fused_finish) args.fin.gen = nullptr;  // only fused launches count in the parity tickets
     const cudaError_t e = y ? dispatch_pass1<Op, true>(args, t, st) : dispatch_pass1<Op, false>(args, t, st);
     UCG_CUDA(e);
     UCG_LAUNCHED();

@@ -74,6 +74,28 @@ def main():
         report["cases"].append({"P": P, "op": op, "exchange": "p2p-graph", "ok": ok, "got": r, "want": float(want)})
         report["ok"] &= ok
         pipe.close()
+    # long chains of repeated steps (early-stream mode: each step launches
+    # its successor at its first instruction; parity start tickets): eager
+    # chains and graph replays at the 8-GPU shard geometry (8 partitions per
+    # rank) and a single-finisher table — a ticket drawn out of order would
+    # stall a rank until the 30 s trap
+    for (P, total, op, eager, graph) in [(8 * world, (1 << 21) * world, "sum", 300, 60),
+                                         (4, 1 << 20, "max", 600, 100)]:
+        lens = partition_sizes(total, P)
+        pipe = MapReducePipeline(lens, op=op, fused=True, world=world, rank=rank, exchange="p2p")
+        partials = [O.tree_reduce(O.map_affine(O.fill_uniform(1000 + p, lens[p]), 2.0, 1.0)
+                                  if not (p == P // 2) else _planted(p, lens[p]), op) for p in range(P)]
+        want = O.tree_reduce(np.array(partials, np.float32), op)
+        for _ in range(eager):
+            pipe.step()
+        ok = O.f32_bits(np.float32(pipe.result.item())) == O.f32_bits(want)
+        for _ in range(4):
+            pipe.result.fill_(float("nan"))
+            ok &= O.f32_bits(np.float32(pipe.graph_step(graph).item())) == O.f32_bits(want)
+        ok &= pipe.exchange_error() == 0
+        report["cases"].append({"P": P, "op": op, "exchange": "p2p-chains", "ok": ok, "want": float(want)})
+        report["ok"] &= ok
+        pipe.close()
     # C3 sharded: map_cl(pi) + reduce_cl(isum2), the rank totals exchanged
     # inside the counting kernel over NVLink; T = world - 1 leaves one rank
     # without tasks (it still joins the exchange)

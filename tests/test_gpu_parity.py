@@ -624,3 +624,28 @@ def test_consecutive_steps_early_mode(cuda, lens, op):
     assert O.f32_bits(pipe2.result.cpu().numpy()[0]) == O.f32_bits(O.tree_reduce(wp3, op))
     pipe.close()
     pipe2.close()
+
+
+@pytest.mark.parametrize("lens", [[1 << 18] * 4, [1 << 21] * 8, [5000] * 300])
+def test_long_step_chains(cuda, lens):
+    """Thousands of chained repeated steps (each launching its successor at
+    its first instruction, parity start tickets) and graph replays of long
+    chains end bit-exact: a ticket drawn out of order would stall a grid
+    until the 30 s trap and fail the launch."""
+    from paper_1505_01120_b200.pipeline import MapReducePipeline
+
+    pipe = MapReducePipeline(lens, op="sum", plant_max=False)
+    p = np.array([O.tree_reduce(O.map_affine(O.fill_uniform(1000 + k, n), 2.0, 1.0), "sum")
+                  for k, n in enumerate(lens)], np.float32)
+    want = O.tree_reduce(p, "sum")
+    for _ in range(3000 if sum(lens) <= (1 << 20) else 500):
+        pipe.step()
+    torch.cuda.synchronize()
+    assert O.f32_bits(pipe.result.cpu().numpy()[0]) == O.f32_bits(want)
+    for _ in range(3):
+        pipe.result.fill_(float("nan"))
+        r = pipe.graph_step(101)
+        torch.cuda.synchronize()
+        assert O.f32_bits(r.cpu().numpy()[0]) == O.f32_bits(want)
+    assert np.array_equal(_bits(pipe.partials), p.view(np.uint32))
+    pipe.close()
