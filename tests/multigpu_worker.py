@@ -18,12 +18,24 @@ from paper_1505_01120_b200.pipeline import MapReducePipeline, partition_sizes  #
 
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
-    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
-    report = {"rank": rank, "ok": True, "cases": []}
+    # UCG_SHARED_GPU=1: every rank on cuda:0 (a one-GPU box). The fused
+    # exchange is unchanged — IPC-mapped regions of another process, epoch-
+    # tagged stores — and the ranks' kernels interleave by time slicing;
+    # torch.distributed (gloo) only carries the IPC handles. NCCL cases skip
+    # (NCCL refuses two ranks on one device).
+    shared = os.environ.get("UCG_SHARED_GPU") == "1"
+    dev = 0 if shared else int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    report = {"rank": rank, "ok": True, "cases": [], "shared_gpu": shared}
     for (P, total, op, fused, exchange) in [(8, 1 << 20, "sum", True, "p2p"), (7, 300001, "max", True, "p2p"),
                                             (64, 1 << 22, "sum", False, "p2p"), (5, 100000, "sum", True, "nccl"),
                                             (3, 50000, "max", False, "nccl")]:
+        if shared and exchange == "nccl":
+            continue
         lens = partition_sizes(total, P)
         pipe = MapReducePipeline(lens, op=op, fused=fused, world=world, rank=rank, exchange=exchange)
         for _ in range(3):  # repeated steps exercise the epoch flags
@@ -41,6 +53,8 @@ def main():
     # alone (ucg_reduce_cl_xchg_f32) — p2p — or the NCCL all-gather
     for (P, total, op, exchange) in [(16, 1 << 22, "sum", "p2p"), (7, 300001, "max", "p2p"),
                                      (16, 1 << 22, "sum", "nccl")]:
+        if shared and exchange == "nccl":
+            continue
         lens = partition_sizes(total, P)
         pipe = MapReducePipeline(lens, op=op, fused=True, world=world, rank=rank, exchange=exchange)
         partials = [O.tree_reduce(O.map_affine(O.fill_uniform(1000 + p, lens[p]), 2.0, 1.0)
@@ -79,8 +93,10 @@ def main():
     # chains and graph replays at the 8-GPU shard geometry (8 partitions per
     # rank) and a single-finisher table — a ticket drawn out of order would
     # stall a rank until the 30 s trap
-    for (P, total, op, eager, graph) in [(8 * world, (1 << 21) * world, "sum", 300, 60),
-                                         (4, 1 << 20, "max", 600, 100)]:
+    chains = [(8 * world, (1 << 21) * world, "sum", 300, 60), (4, 1 << 20, "max", 600, 100)]
+    if shared:  # every exchange waits for the other rank's time slice
+        chains = [(8 * world, (1 << 21) * world, "sum", 20, 8), (4, 1 << 20, "max", 30, 10)]
+    for (P, total, op, eager, graph) in chains:
         lens = partition_sizes(total, P)
         pipe = MapReducePipeline(lens, op=op, fused=True, world=world, rank=rank, exchange="p2p")
         partials = [O.tree_reduce(O.map_affine(O.fill_uniform(1000 + p, lens[p]), 2.0, 1.0)
