@@ -33,13 +33,15 @@ def test_sharded_pipeline_bit_identical():
 
 
 @pytest.mark.gpu
-def test_sharded_two_ranks_one_gpu():
-    """The sharded path at world size 2 on ONE GPU (both ranks on cuda:0):
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_ranks_one_gpu(world):
+    """The sharded path at world size 2 and 8 on ONE GPU (every rank on cuda:0):
     the same IPC-mapped regions, epoch-tagged 64-bit stores and graph-
     replayed steps as across GPUs, the two processes' kernels interleaved by
     time slicing; torch.distributed (gloo) only carries the IPC handles. Every
     rank's partials and result must equal the single-GPU bits — the multi-
-    rank protocol checked on a one-GPU box."""
+    rank protocol (8 ranks: the driver's 8-GPU geometry) checked on a
+    one-GPU box."""
     import json
     import os
     import re
@@ -52,14 +54,14 @@ def test_sharded_two_ranks_one_gpu():
     if mode and mode.lower() != "default":
         pytest.skip(f"compute mode {mode}: one context per GPU")
     env = dict(os.environ, UCG_SHARED_GPU="1")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29547",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(29547 + world),
                         str(ROOT / "tests" / "multigpu_worker.py")], capture_output=True, text=True, timeout=600,
                        env=env)
     reports = [json.JSONDecoder().raw_decode(r.stdout, m.end())[0] for m in re.finditer(r"MULTIGPU ", r.stdout)]
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0, r.stderr[-3000:]
-    assert sorted(d["rank"] for d in reports) == [0, 1], r.stdout[-3000:]
+    assert sorted(d["rank"] for d in reports) == list(range(world)), r.stdout[-3000:]
     assert all(d["shared_gpu"] for d in reports)
     bad = [(d["rank"], c) for d in reports for c in d["cases"] if not c["ok"]]
     assert not bad, bad
