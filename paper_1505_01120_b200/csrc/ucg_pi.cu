@@ -28,7 +28,6 @@ struct PiTasks {
   uint64_t samples[kMaxTasks];
   uint64_t first_unit[kMaxTasks + 1];
   uint32_t ntasks;
-  uint32_t p2, p4;  // 2 and 4, opaque to the compiler (shr_fma)
 };
 
 // 64-bit x + c with the add on the FMA pipe (IMAD.WIDE.U32 + IMAD): the
@@ -41,43 +40,21 @@ __device__ __forceinline__ uint64_t add64_fma(uint64_t x, uint64_t c) {
   return (uint64_t(hi) << 32) | uint32_t(lo);
 }
 
-// x >> s for a 32-bit word as the high word of x * 2^(32-s) (IMAD.HI on the
-// FMA pipe); `pow` is 2^(32-s) from a kernel parameter, so the compiler
-// cannot turn it back into a shift on the ALU pipe
-__device__ __forceinline__ uint32_t shr_fma(uint32_t x, uint32_t pow) {
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(pow));
-  return r;
-}
-
 // High 32 bits of mix64(z): the last step z ^ (z >> 31) only feeds bit 63
 // of z into the high word, so hi32 = hi(z) ^ (hi(z) >> 31).
-// kFinal / kFirst: do the final h >> 31 / the first step's high-word >> 30 as
-// IMAD.HI on the FMA pipe instead of SHF on the ALU pipe (the kernel is
-// ALU-pipe bound: 29 ALU against 17 FMA-pipe operations per sample).
-template <bool kFinal, bool kFirst>
-__device__ __forceinline__ uint32_t mix64_hi(uint64_t z, uint32_t p2, uint32_t p4) {
-  if constexpr (kFirst) {
-    const uint32_t lo = uint32_t(z), hi = uint32_t(z >> 32);
-    const uint32_t slo = __funnelshift_r(lo, hi, 30), shi = shr_fma(hi, p4);
-    z = ((uint64_t(hi ^ shi) << 32) | (lo ^ slo)) * 0xBF58476D1CE4E5B9ull;
-  } else {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  }
+__device__ __forceinline__ uint32_t mix64_hi(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   const uint32_t h = uint32_t(z >> 32);
-  return h ^ (kFinal ? shr_fma(h, p2) : h >> 31);
+  return h ^ (h >> 31);
 }
 
 // Exact reference test on the FP64 pipe (separate from the integer ALU):
 // x*x = fl(a^2)*2^-64 exactly, so fl(fl(x*x)+fl(y*y)) <= 1 is
 // fl(fl(a^2)+fl(b^2)) <= 2^64 with a, b converted exactly to double.
-// kHi (bit mask, UCG_PI_HI): 1 = both final shifts on the FMA pipe, 2 = the
-// first mix's first-step shift, 4 = the second mix's.
-template <int kHi = 0>
-__device__ __forceinline__ uint32_t pi_hit(uint64_t s0, uint32_t p2 = 2, uint32_t p4 = 4) {
-  const uint32_t a = mix64_hi<(kHi & 1) != 0, (kHi & 2) != 0>(add64_fma(s0, kGamma), p2, p4);
-  const uint32_t b = mix64_hi<(kHi & 1) != 0, (kHi & 4) != 0>(add64_fma(s0, 2 * kGamma), p2, p4);
+__device__ __forceinline__ uint32_t pi_hit(uint64_t s0) {
+  const uint32_t a = mix64_hi(add64_fma(s0, kGamma));
+  const uint32_t b = mix64_hi(add64_fma(s0, 2 * kGamma));
   const double da = __uint2double_rn(a), db = __uint2double_rn(b);
   return __dadd_rn(__dmul_rn(da, da), __dmul_rn(db, db)) <= 18446744073709551616.0 ? 1u : 0u;
 }
@@ -158,7 +135,6 @@ __device__ void pi_exchange(const PiXchg& x, unsigned long long* total) {
   }
 }
 
-template <int kHi>
 __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTasks tasks, uint64_t nunits,
                                                    unsigned long long* __restrict__ hits,
                                                    unsigned long long* __restrict__ total, const PiXchg xg) {
@@ -179,10 +155,9 @@ __global__ void __launch_bounds__(kPiThreads) k_pi(const __grid_constant__ PiTas
     uint64_t m = gid * kGamma;
     const uint64_t mstep = uint64_t(kPiThreads) * kGamma;
     if (end - base == (1ull << kUnitLog2)) {
-      const uint32_t p2 = tasks.p2, p4 = tasks.p4;
 #pragma unroll 4
       for (int i = 0; i < (1 << kUnitLog2) / kPiThreads; ++i) {
-        cnt += pi_hit<kHi>(seed ^ m, p2, p4);
+        cnt += pi_hit(seed ^ m);
         m = add64_fma(m, mstep);
       }
     } else {
@@ -229,23 +204,6 @@ extern "C" int ucg_pi_flags(uint64_t seed, uint64_t samples, uint8_t* flags, voi
 }
 
 namespace {
-// UCG_PI_HI (A/B runs): which SplitMix64 high-word shifts run as IMAD.HI on
-// the FMA pipe (bit mask, see pi_hit); 0 = all on the ALU pipe
-using PiKernel = void (*)(PiTasks, uint64_t, unsigned long long*, unsigned long long*, PiXchg);
-PiKernel pi_kernel() {
-  static const PiKernel k = [] {
-    const char* e = getenv("UCG_PI_HI");
-    switch (e ? atoi(e) : 0) {
-      case 1: return PiKernel(k_pi<1>);
-      case 3: return PiKernel(k_pi<3>);
-      case 7: return PiKernel(k_pi<7>);
-      case 5: return PiKernel(k_pi<5>);
-      default: return PiKernel(k_pi<0>);
-    }
-  }();
-  return k;
-}
-
 int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, int64_t* hits_out, int64_t* total_out,
               ucg_xchg* xg, void* stream) {
   if (int rc = check_device()) return rc;
@@ -272,8 +230,6 @@ int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, i
     const uint32_t nt = uint32_t(std::min<uint64_t>(kMaxTasks, ntasks - t0));
     PiTasks p;
     p.ntasks = nt;
-    p.p2 = 2;
-    p.p4 = 4;
     p.first_unit[0] = 0;
     for (uint32_t i = 0; i < nt; ++i) {
       p.seed[i] = seeds[t0 + i];
@@ -288,8 +244,8 @@ int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, i
     const bool last_chunk = t0 + kMaxTasks >= ntasks;
     const PiXchg xl = last_chunk ? xa : PiXchg{};
     exchanged |= last_chunk && xa.peers;
-    pi_kernel()<<<grid, kPiThreads, 0, st>>>(p, nunits, reinterpret_cast<unsigned long long*>(hits_out + t0),
-                                             reinterpret_cast<unsigned long long*>(total_out), xl);
+    k_pi<<<grid, kPiThreads, 0, st>>>(p, nunits, reinterpret_cast<unsigned long long*>(hits_out + t0),
+                                      reinterpret_cast<unsigned long long*>(total_out), xl);
     UCG_LAUNCHED();
   }
   if (xa.peers && !exchanged) {
@@ -297,10 +253,8 @@ int pi_launch(const uint64_t* seeds, const uint64_t* samples, uint64_t ntasks, i
     // the exchange, with its total as it stands
     PiTasks p;
     p.ntasks = 0;
-    p.p2 = 2;
-    p.p4 = 4;
     p.first_unit[0] = 0;
-    pi_kernel()<<<1, kPiThreads, 0, st>>>(p, 0, nullptr, reinterpret_cast<unsigned long long*>(total_out), xa);
+    k_pi<<<1, kPiThreads, 0, st>>>(p, 0, nullptr, reinterpret_cast<unsigned long long*>(total_out), xa);
     UCG_LAUNCHED();
   }
   return UCG_OK;
