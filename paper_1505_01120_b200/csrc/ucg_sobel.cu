@@ -712,12 +712,14 @@ int ucg_sobel_bands_u8(const uint8_t* in, const uint64_t* in_off, uint8_t* out, 
       const char* e = getenv("UCG_SOBEL_SLOTS");
       return e && atoi(e) == 6 ? 6 : 4;
     }();
-    // row streaming (A/B only): 16 or 8 columns per lane, integer or fp16 form
-    const bool half = arith != 0;
-    auto kern = half ? (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, 1> : k_sobel_rows<5, 4, 16, 1>)
-                                   : (slots == 6 ? k_sobel_rows<8, 6, 8, 1> : k_sobel_rows<8, 4, 8, 1>))
-                     : (cols == 16 ? (slots == 6 ? k_sobel_rows<5, 6, 16, 0> : k_sobel_rows<5, 4, 16, 0>)
-                                   : (slots == 6 ? k_sobel_rows<8, 6, 8, 0> : k_sobel_rows<8, 4, 8, 0>));
+    // row streaming (A/B only): 16 or 8 columns per lane (4 row slots), or
+    // 16 columns with 6 slots; integer, fp16 or mixed form
+    auto kern = cols == 8 ? (arith == 0 ? k_sobel_rows<8, 4, 8, 0> : k_sobel_rows<8, 4, 8, 2>)
+                : slots == 6 ? (arith == 0 ? k_sobel_rows<5, 6, 16, 0> : k_sobel_rows<5, 6, 16, 2>)
+                : arith == 0 ? k_sobel_rows<5, 4, 16, 0>
+                : arith == 1 ? k_sobel_rows<5, 4, 16, 1>
+                : arith == 3 ? k_sobel_rows<5, 4, 16, 3>
+                             : k_sobel_rows<5, 4, 16, 2>;
     const uint32_t smem = cols == 16 ? (slots == 6 ? sobel_rows_smem<6, 16>() : sobel_rows_smem<4, 16>())
                                      : (slots == 6 ? sobel_rows_smem<6, 8>() : sobel_rows_smem<4, 8>());
     const uint32_t seg_cols = 32u * uint32_t(cols);
