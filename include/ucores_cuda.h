@@ -125,7 +125,9 @@ int ucg_fill_bytes_u8(uint8_t* out, uint64_t n, uint64_t seed, uint64_t first, v
  * at float offset begin[s] (multiple of 4) with len[s] floats. The table is
  * uploaded once (synchronously) on the current device and reused by every
  * launch over that layout on that device; it also carries the launches'
- * work-item counters, so it serves one launch at a time. */
+ * work-item counters (two sets, used by alternate launches), so it serves
+ * one stream at a time: launches on it are stream-ordered, and a repeated
+ * step may overlap only the step before it (see ucg_segtab_scratch_floats). */
 typedef struct ucg_segtab ucg_segtab;
 int ucg_segtab_create(const uint64_t* begin, const uint64_t* len, uint64_t nseg, ucg_segtab** out);
 int ucg_segtab_destroy(ucg_segtab* t);
