@@ -268,11 +268,12 @@ def workload_config(args, world: int) -> dict:
         "l2": f"inputs larger than L2 ({n * 4 // world / 2**30:.2f} GiB x per GPU)",
         "timed_launch": ("the K steps launched one by one" if getattr(args, "no_graph", False)
                          else "the K steps replayed from one CUDA graph of K one-kernel steps"),
-        "step_overlap": ("none (UCG_NO_EARLY)" if os.environ.get("UCG_NO_EARLY") else
-                         "consecutive steps overlap: step k+1 launches at step k's first instruction and streams "
-                         "on the SM slots step k's CTAs leave, while step k finishes its trees, stage 2 and exchange "
-                         "(alternate counter/scratch halves); every step does the whole map + trees + stage 2"),
     }
+
+
+STEP_OVERLAP = ("consecutive steps overlap: step k+1 launches at step k's first instruction and streams on the SM "
+                "slots step k's CTAs leave, while step k finishes its trees, stage 2 and exchange (alternate "
+                "counter/scratch halves); every step does the whole map + trees + stage 2")
 
 
 GOLDEN_FULL = ROOT / "tests" / "golden" / "ref_golden_full.json"
@@ -561,6 +562,7 @@ def our_arm(args, world, rank, local):
             "cpu_baseline": cpu,
             "e2e_reference_api": engine_e2e,
             "gpu_launches": launches,
+            "step_overlap": "none (UCG_NO_EARLY)" if os.environ.get("UCG_NO_EARLY") else STEP_OVERLAP,
             "clocks": clk.summary(),
             "result": result,
             "parity": parity,
