@@ -405,7 +405,7 @@ template <int kTerms>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2_threads<kTerms>(), 1)
     k_gemm_tf32_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
-                    float* __restrict__ C, int n, int nchunks) {
+                    float* __restrict__ C, int n, int nchunks, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[S2], empty[S2], tfull[2], tempty[2];
@@ -456,10 +456,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2_threads<kTerms
       for (int t = pair; t < ntiles; t += npairs) {
         int mb, nb;
         {  // grouped raster over 256 x 256 tiles
-          const int per_group = kGroupM * tiles_n;
+          const int per_group = group_m * tiles_n;
           const int g = t / per_group, idx = t % per_group;
-          const int gm = min(kGroupM, tiles_m - g * kGroupM);
-          mb = g * kGroupM + idx % gm;
+          const int gm = min(group_m, tiles_m - g * group_m);
+          mb = g * group_m + idx % gm;
           nb = idx / gm;
         }
         const int m0 = mb * 256 + int(rank) * 128, n0 = nb * 256 + int(rank) * 128;
@@ -515,10 +515,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2_threads<kTerms
       const int t = pair + (u / nchunks) * npairs;
       int mb, nb;
       {
-        const int per_group = kGroupM * tiles_n;
+        const int per_group = group_m * tiles_n;
         const int g = t / per_group, idx = t % per_group;
-        const int gm = min(kGroupM, tiles_m - g * kGroupM);
-        mb = g * kGroupM + idx % gm;
+        const int gm = min(group_m, tiles_m - g * group_m);
+        mb = g * group_m + idx % gm;
         nb = idx / gm;
       }
       const uint32_t acc = i & 1;
@@ -567,10 +567,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2_threads<kTerms
       if (chunk + 1 == nchunks) {
         int mb, nb;
         {
-          const int per_group = kGroupM * tiles_n;
+          const int per_group = group_m * tiles_n;
           const int g = t / per_group, idx = t % per_group;
-          const int gm = min(kGroupM, tiles_m - g * kGroupM);
-          mb = g * kGroupM + idx % gm;
+          const int gm = min(group_m, tiles_m - g * group_m);
+          mb = g * group_m + idx % gm;
           nb = idx / gm;
         }
         float4* dst = reinterpret_cast<float4*>(C + size_t(mb * 256 + int(rank) * 128 + lg * 32 + lane) * n +
@@ -609,6 +609,20 @@ __global__ void __launch_bounds__(256) k_split_tf32(const float4* __restrict__ x
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() { return tmap_encode_fn(); }
+
+// m-blocks (of 256 rows) per raster group of the CTA-pair kernel: 8 — the
+// 74 concurrent tile pairs then cover ~8 x 9 tiles, so fewer A/B panels
+// stream at once (ncu DRAM reads 7.1 vs 8.2 GB per fp32-faithful 8192^3
+// launch at 16; C5 line 219.8-220.1 vs 218.3-218.4 TF/s, same box;
+// UCG_GEMM_GROUP for A/B runs)
+int gemm_group_m() {
+  static const int g = [] {
+    const char* e = getenv("UCG_GEMM_GROUP");
+    const int v = e ? atoi(e) : 8;
+    return v > 0 ? v : 8;
+  }();
+  return g;
+}
 
 int make_map(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
              uint32_t box_outer, CUtensorMapSwizzle swz) {
@@ -657,7 +671,7 @@ extern "C" int ucg_gemm_tf32(const float* A, const float* B, float* C, uint64_t 
     const uint64_t ntiles = (n / 256) * (n / 256);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count() / 2))) * 2;
     k_gemm_tf32_2sm<1><<<grid, gemm2_threads<1>(), SMEM2_BYTES, as_stream(stream)>>>(tmA, tmB, tmA, tmB, C, int(n),
-                                                                                      1);
+                                                                                      1, gemm_group_m());
   } else {
     const uint64_t ntiles = (n / BM) * (n / BN);
     const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(sm_count())));
@@ -704,7 +718,7 @@ extern "C" int ucg_gemm_f32(const float* A, const float* B, float* C, uint64_t n
     if (const char* e = getenv("UCG_GEMM_KCHUNK")) kchunk = atoi(e);
     if (kchunk < BK || kchunk % BK || n % uint64_t(kchunk)) kchunk = int(n);
     k_gemm_tf32_2sm<3><<<grid, gemm2_threads<3>(), SMEM2_BYTES, st>>>(tmAh, tmBh, tmAl, tmBl, C, int(n),
-                                                                     int(n / kchunk));
+                                                                     int(n / kchunk), gemm_group_m());
     UCG_LAUNCHED();
   }
   UCG_CUDA(cudaFreeAsync(w, st));
