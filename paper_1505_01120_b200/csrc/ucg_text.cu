@@ -146,6 +146,16 @@ __global__ void __launch_bounds__(256) k_word_flags_claim(const uint8_t* __restr
     const uint32_t prev = i > 0 ? (delim_mask(in[16 * i - 1]) & 1u) : 1u;
     __stcs(dst + i, word_flags16(v, prev));
   }
+  // ctr[1] counts CTAs out: the last one returns the claim pair to zero for
+  // its next user (claim_pair_selfreset: no memset launch per call)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1ull) == gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_word_flags_bytes(const uint8_t* __restrict__ in, uint8_t* __restrict__ flags,
@@ -180,11 +190,17 @@ extern "C" int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* f
       const unsigned grid = unsigned(std::min<uint64_t>((warps + 7) / 8, uint64_t(sm_count()) * 8));
       k_word_flags<4><<<grid, 256, 0, st>>>(bytes, flags, n16);
     } else {
-      unsigned long long* ctr = claim_counter();
+      unsigned long long* ctr = claim_pair_selfreset();  // zero at launch, re-zeroed by the last CTA
       if (!ctr) return fail(UCG_ERR_CUDA, "word flags: counter allocation failed");
-      UCG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st));
+      // UCG_WC_WU (A/B): 16-byte words per lane per block, 4 (2 KB blocks,
+      // 8 per claim) or 8 (4 KB blocks, 4 per claim: twice the bytes in flight)
+      static const int wu = [] {
+        const char* e = getenv("UCG_WC_WU");
+        return e && atoi(e) == 8 ? 8 : 4;
+      }();
       const unsigned grid = unsigned(std::min<uint64_t>((warps / 8 + 7) / 8 + 1, uint64_t(sm_count()) * 8));
-      k_word_flags_claim<4, 8><<<grid, 256, 0, st>>>(bytes, flags, n16, ctr);
+      if (wu == 8) k_word_flags_claim<8, 4><<<grid, 256, 0, st>>>(bytes, flags, n16, ctr);
+      else k_word_flags_claim<4, 8><<<grid, 256, 0, st>>>(bytes, flags, n16, ctr);
     }
     UCG_LAUNCHED();
     done = n16 * 16;
