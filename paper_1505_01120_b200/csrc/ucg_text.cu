@@ -179,8 +179,8 @@ extern "C" int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* f
   uint64_t done = 0;
   if (aligned16(bytes) && aligned16(flags) && n >= 16) {
     const uint64_t n16 = n / 16;
-    // default: claimed 16 KB units (1 GiB in 0.394 ms, 0.85 of HBM);
-    // UCG_WC_VARIANT=1: grid-stride blocks (0.406 ms)
+    // default: claimed 16 KB units (round 1: 1 GiB in 0.394 ms, 0.85 of
+    // HBM); UCG_WC_VARIANT=1: grid-stride blocks (0.406 ms)
     static const int variant = [] {
       const char* e = getenv("UCG_WC_VARIANT");
       return e ? atoi(e) : 0;
@@ -192,11 +192,12 @@ extern "C" int ucg_word_start_flags(const uint8_t* bytes, uint64_t n, uint8_t* f
     } else {
       unsigned long long* ctr = claim_pair_selfreset();  // zero at launch, re-zeroed by the last CTA
       if (!ctr) return fail(UCG_ERR_CUDA, "word flags: counter allocation failed");
-      // UCG_WC_WU (A/B): 16-byte words per lane per block, 4 (2 KB blocks,
-      // 8 per claim) or 8 (4 KB blocks, 4 per claim: twice the bytes in flight)
+      // 16-byte words per lane per block: 8 (default; 4 KB blocks, 4 per
+      // claim: twice the bytes in flight of 4 — 1 GiB in 333.5 vs 346.9 us,
+      // 0.985 vs 0.946 of the copy peak, same box) or 4 (UCG_WC_WU=4, A/B)
       static const int wu = [] {
         const char* e = getenv("UCG_WC_WU");
-        return e && atoi(e) == 8 ? 8 : 4;
+        return e && atoi(e) == 4 ? 4 : 8;
       }();
       const unsigned grid = unsigned(std::min<uint64_t>((warps / 8 + 7) / 8 + 1, uint64_t(sm_count()) * 8));
       if (wu == 8) k_word_flags_claim<8, 4><<<grid, 256, 0, st>>>(bytes, flags, n16, ctr);
