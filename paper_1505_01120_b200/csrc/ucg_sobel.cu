@@ -4,14 +4,15 @@
 // the image columns (oracle/ucores_oracle.c orc_sobel_band_u8). Separable
 // form: with dh(c) = p(c+1)-p(c-1) and sh(c) = p(c-1)+2p(c)+p(c+1) per row,
 // Gx = dh(r0)+2dh(r1)+dh(r2) and Gy = sh(r2)-sh(r0). Arithmetic is packed two
-// pixels per 32-bit register (biased 16-bit halves, byte permutes to build
-// the neighbour vectors, sm_100 packed 16x2 min/max), ~7 integer ops/pixel.
+// pixels per 32-bit register (16-bit halves, byte permutes build the
+// neighbour vectors); by default the halves are read as fp16 subnormals and
+// added exactly with HADD2/HFMA2 (see word_terms / out_pair below).
 //
-// Data movement: one thread owns 16 consecutive columns (one 128-bit load
-// per input row) and walks down a strip of kStrip output rows keeping the
-// 3-row window in registers, so each input row is read from HBM once (plus
-// 2 halo rows per strip); the left/right neighbour bytes come from the
-// adjacent lanes by shuffle. One 128-bit store per output row.
+// Three kernels: the default TMA-tiled persistent kernel (k_sobel_tma, tiles
+// claimed from a self-resetting counter pair), a row-streaming TMA kernel
+// (k_sobel_rows, A/B) and a register-streaming kernel without TMA (k_sobel,
+// below: one thread owns 16 consecutive columns and walks down a strip of
+// kStrip output rows, the neighbour bytes by shuffle; A/B).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kSobelThreads)
 // 66 x 256 input rows plus 16-byte side boxes at x-16 and x+256 into shared
 // memory; side boxes that fall outside the image are zero-filled by the TMA
 // unit, which is exactly the zero-outside-columns rule. Persistent CTAs double
-// buffer: the tile after next is requested as soon as a buffer is free. Each
+// buffer: the next tile is requested as soon as a buffer is free. Each
 // of the 128 threads owns 16 columns x 8 output rows (10 input rows, 3-row
 // window in registers), reads its bytes with LDS.128 and the neighbour bytes
 // from the side columns, and stores 16 output bytes per row.
