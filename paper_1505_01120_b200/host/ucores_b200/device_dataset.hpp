@@ -318,7 +318,7 @@ class DeviceEngine {
 
   /// Engine::map_cl (engine.hpp:54-85): axpb, psum, pmax, pi, sobel, matmul.
   DeviceDataset map_cl(const DeviceDataset& d, const std::string& kernel) {
-    TraceRange trace("ucores.map_cl/" + kernel);
+    TraceRange trace("ucores.map_cl:" + kernel);
     return unary(d, kernel, false);
   }
 
@@ -326,7 +326,7 @@ class DeviceEngine {
   /// partitions: axpb, psum, pmax, sobel (pi / matmul fail as in the
   /// reference unless a partition holds exactly one element).
   DeviceDataset map_cl_partition(const DeviceDataset& d, const std::string& kernel) {
-    TraceRange trace("ucores.map_cl_partition/" + kernel);
+    TraceRange trace("ucores.map_cl_partition:" + kernel);
     for (std::size_t p = 0; p < d.parts_.size(); ++p) {
       if (d.parts_[p].sizes.empty()) {
         fail(p, "map_parameters: element kind mismatch, have bytes (empty partition concatenates to an empty "
@@ -338,7 +338,7 @@ class DeviceEngine {
 
   /// Engine::reduce_cl (engine.hpp:121-192): sum2, max2, vectoradd, isum2.
   ucores::Element reduce_cl(const DeviceDataset& d, const std::string& kernel) {
-    TraceRange trace("ucores.reduce_cl/" + kernel);
+    TraceRange trace("ucores.reduce_cl:" + kernel);
     const bool i64 = kernel == "isum2";
     if (!i64 && kernel != "sum2" && kernel != "max2" && kernel != "vectoradd") {
       throw ucores::UnknownKernel("no device reduce_cl body for kernel '" + kernel + "'");

@@ -2,7 +2,8 @@
 // tracing): the driver's waves and per-GPU batches (seam A), the executor's
 // run phase (seam B), DeviceEngine's operators and transfers. They show up in
 // nsys timelines and filter ncu captures (`ncu --nvtx --nvtx-include
-// "ucores.map_cl/"`). nvtx3 is header-only and binds a tool lazily: with no
+// "ucores.map_cl_partition:psum/"`; names avoid '/', ncu's nesting
+// separator). nvtx3 is header-only and binds a tool lazily: with no
 // tool attached a range is one predicted branch.
 #pragma once
 
