@@ -56,6 +56,39 @@ def _soak(fn, warmup, barrier, seconds=1.0):
     barrier()
 
 
+class _Duplex:
+    """One end-to-end step in pieces: piece i's upload (copy-in stream), its
+    kernel (the current stream) and its download (copy-out stream), so the
+    uploads of later pieces overlap the downloads of earlier ones on the two
+    copy engines (PCIe is full duplex). Every step still moves all of its
+    inputs up and all of its outputs down."""
+
+    def __init__(self, dev):
+        self.s_in = torch.cuda.Stream(device=dev)
+        self.s_out = torch.cuda.Stream(device=dev)
+
+    def step(self, npieces, h2d, run, d2h):
+        cur = torch.cuda.current_stream()
+        self.s_in.wait_stream(cur)
+        ups = []
+        with torch.cuda.stream(self.s_in):
+            for i in range(npieces):
+                h2d(i)
+                e = torch.cuda.Event()
+                e.record(self.s_in)
+                ups.append(e)
+        for i in range(npieces):
+            cur.wait_event(ups[i])
+            run(i)
+            e = torch.cuda.Event()
+            e.record(cur)
+            self.s_out.wait_event(e)
+            with torch.cuda.stream(self.s_out):
+                d2h(i)
+        cur.wait_stream(self.s_out)
+        cur.synchronize()
+
+
 def _max_over_ranks(vals, world, dev):
     if world == 1:
         return vals
@@ -233,11 +266,27 @@ def run(args, world, rank, local):
         host_in = torch.empty_like(inp, device="cpu").pin_memory()
         host_out = torch.empty_like(out, device="cpu").pin_memory()
 
-        def e2e():
-            inp.copy_(host_in, non_blocking=True)
-            fn()
-            host_out.copy_(out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        host_in.copy_(inp)
+        # e2e in pieces of 8 bands: uploads overlap downloads (_Duplex)
+        duplex, per_piece = _Duplex(dev), 8
+        npieces = (ln + per_piece - 1) // per_piece if ln else 0
+        ib, ob = (R + 2) * W, R * W
+
+        def h2d(i):
+            b0, b1 = i * per_piece, min(ln, (i + 1) * per_piece)
+            inp[b0 * ib:b1 * ib].copy_(host_in[b0 * ib:b1 * ib], non_blocking=True)
+
+        def run(i):
+            b0, b1 = i * per_piece, min(ln, (i + 1) * per_piece)
+            ops.sobel_bands(inp, in_off[b0:b1], out, out_off[b0:b1], [R] * (b1 - b0), W)
+
+        def d2h(i):
+            b0, b1 = i * per_piece, min(ln, (i + 1) * per_piece)
+            host_out[b0 * ob:b1 * ob].copy_(out[b0 * ob:b1 * ob], non_blocking=True)
+
+        e2e = lambda: duplex.step(npieces, h2d, run, d2h)  # noqa: E731
+        e2e()
+        e2e_matches = bool(torch.equal(host_out, out.cpu()))
         e2e_ms = _timed(e2e, k, barrier)
         ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
         if rank == 0:
@@ -249,7 +298,9 @@ def run(args, world, rank, local):
         achieved = algo / (ms * 1e-3) / 1e9
         line = _line(args, world, "c4", CONFIGS[3], H * W / (ms * 1e-3), "pixels/s", ms, launches, clk,
                      {"value": H * W / (e2e_ms * 1e-3), "unit": "pixels/s",
-                      "h2d_bytes_per_step": nb * (R + 2) * W, "d2h_bytes_per_step": H * W},
+                      "h2d_bytes_per_step": nb * (R + 2) * W, "d2h_bytes_per_step": H * W,
+                      "pipeline": "pieces of 8 bands: upload, kernel, download; uploads overlap downloads",
+                      "matches_device_result": e2e_matches},
                      {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                       "frac": achieved / peak_hbm, "traffic": _traffic("sobel_dram_bytes", ln / nb),
                       "peak_kind": peak_kind, "algorithmic_bytes_per_launch": algo},
@@ -301,13 +352,38 @@ def run(args, world, rank, local):
         hC = torch.empty_like(Cm, device="cpu").pin_memory()
         hA.copy_(A)
 
+        # e2e: per partition A, B up, the product, C down — double-buffered, so
+        # partition i+1's upload (copy-in stream) runs under partition i's
+        # GEMM and download (copy-out stream)
+        Ab, Bb, Cb = [A, torch.empty_like(A)], [Bm, torch.empty_like(Bm)], [Cm, torch.empty_like(Cm)]
+        s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
         def e2e():
-            for _ in mine:
-                A.copy_(hA, non_blocking=True)
-                Bm.copy_(hA, non_blocking=True)
-                ops.gemm_f32(A, Bm, Cm, n)
-                hC.copy_(Cm, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            cur = torch.cuda.current_stream()
+            s_in.wait_stream(cur)
+            kdone, ddone = {}, {}
+            for i, _ in enumerate(mine):
+                j = i % 2
+                with torch.cuda.stream(s_in):
+                    if i >= 2:
+                        s_in.wait_event(kdone[i - 2])  # GEMM i-2 has read buffer j
+                    Ab[j].copy_(hA, non_blocking=True)
+                    Bb[j].copy_(hA, non_blocking=True)
+                    up = torch.cuda.Event()
+                    up.record(s_in)
+                cur.wait_event(up)
+                if i >= 2:
+                    cur.wait_event(ddone[i - 2])  # C buffer j downloaded
+                ops.gemm_f32(Ab[j], Bb[j], Cb[j], n)
+                kdone[i] = torch.cuda.Event()
+                kdone[i].record(cur)
+                s_out.wait_event(kdone[i])
+                with torch.cuda.stream(s_out):
+                    hC.copy_(Cb[j], non_blocking=True)
+                    ddone[i] = torch.cuda.Event()
+                    ddone[i].record(s_out)
+            cur.wait_stream(s_out)
+            cur.synchronize()
         e2e_ms = _timed(e2e, max(1, k // 4), barrier)
         ms32, mstf, cub, e2e_ms = _max_over_ranks([ms32, mstf, cub, e2e_ms], world, dev)
         flops = 2.0 * n ** 3 * P
@@ -322,7 +398,9 @@ def run(args, world, rank, local):
         tctf = 2.0 * n ** 3 / (mstf * 1e-3 / nloc) / 1e12
         line = _line(args, world, "c5", CONFIGS[4], flops / (ms32 * 1e-3), "FLOP/s", ms32, launches, clk,
                      {"value": flops / (e2e_ms * 1e-3), "unit": "FLOP/s",
-                      "h2d_bytes_per_step": P * 2 * n * n * 4, "d2h_bytes_per_step": P * n * n * 4},
+                      "h2d_bytes_per_step": P * 2 * n * n * 4, "d2h_bytes_per_step": P * n * n * 4,
+                      "pipeline": "double-buffered partitions: the next A, B upload under this product and its C "
+                                  "download"},
                      {"bound": "tensor", "achieved": tc32, "peak": peak, "unit": "TFLOP/s", "frac": tc32 / peak,
                       "traffic": _traffic("gemm_f32_dram_bytes", 1.0), "traffic_note": "ncu DRAM bytes of one "
                       "8192^3 fp32-faithful launch (profiles/ncu_summary.json r02)",
@@ -416,11 +494,26 @@ def run(args, world, rank, local):
         host_in.copy_(text)
         host_out = torch.empty_like(flags, device="cpu").pin_memory()
 
-        def e2e():
-            text.copy_(host_in, non_blocking=True)
-            fn()
-            host_out.copy_(flags, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        # e2e in pieces of 8 chunks (each ends on a delimiter, so a piece's
+        # flags are exact on their own): uploads overlap downloads (_Duplex)
+        duplex, per_piece = _Duplex(dev), 8 * per
+        npieces = (text.numel() + per_piece - 1) // per_piece if ln else 0
+
+        def h2d(i):
+            text[i * per_piece:(i + 1) * per_piece].copy_(host_in[i * per_piece:(i + 1) * per_piece], non_blocking=True)
+
+        def run(i):
+            ops.word_start_flags(text[i * per_piece:(i + 1) * per_piece], flags[i * per_piece:(i + 1) * per_piece])
+
+        def d2h(i):
+            host_out[i * per_piece:(i + 1) * per_piece].copy_(flags[i * per_piece:(i + 1) * per_piece],
+                                                             non_blocking=True)
+
+        e2e = lambda: duplex.step(npieces, h2d, run, d2h)  # noqa: E731
+        fn()
+        want_flags = flags.cpu()
+        e2e()
+        e2e_matches = bool(torch.equal(host_out, want_flags))
         e2e_ms = _timed(e2e, k, barrier)
         ms, e2e_ms = _max_over_ranks([ms, e2e_ms], world, dev)
         words = int(flags.sum(dtype=torch.int64).item()) if ln else 0
@@ -436,7 +529,9 @@ def run(args, world, rank, local):
         line = _line(args, world, "wc", "WordCount word-start flags over create_from_text chunks (SURVEY 8(f)4)",
                      total / (ms * 1e-3), "bytes/s", ms, launches, clk,
                      {"value": total / (e2e_ms * 1e-3), "unit": "bytes/s", "h2d_bytes_per_step": total,
-                      "d2h_bytes_per_step": total, "note": "text up, flags down (the host tokeniser's input)"},
+                      "d2h_bytes_per_step": total, "note": "text up, flags down (the host tokeniser's input)",
+                      "pipeline": "pieces of 8 chunks: upload, kernel, download; uploads overlap downloads",
+                      "matches_device_result": e2e_matches},
                      {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                       "frac": achieved / peak_hbm, "traffic": _traffic("wordflags_dram_bytes", ln / chunks),
                       "peak_kind": peak_kind, "algorithmic_bytes_per_launch": algo},
