@@ -164,7 +164,10 @@ def run(args, world, rank, local):
         pipe.step()
         torch.cuda.synchronize()
         assert float(pipe.result.item()) == r_graph  # graph replay == eager step, bitwise
-        pipe.setup_host_input(chunks=4)
+        # e2e chunks (UCG_C1_E2E_CHUNKS, A/B): 4 MB of x is one upload's
+        # worth; per-chunk host work (copy, event, launch) costs more than the
+        # overlap gains at this size
+        pipe.setup_host_input(chunks=int(os.environ.get("UCG_C1_E2E_CHUNKS", "1")))
         for _ in range(2):
             pipe.step_from_host()
         e2e_ms = _timed(pipe.step_from_host, k, barrier)
